@@ -1,0 +1,173 @@
+/*
+ * hjb200 -- C ABI of the B200-native block J-Jacobi hot path.
+ *
+ * Drop-in boundary for the reference's ``parallel_jacobi(G, signs,
+ * SolverConfig) -> (G_out, DiagInfo)`` (reference:
+ * pkg/src/hjacobi/parallel.py:255-309), its schedule generator
+ * (strategies.py:143-176) and eigenpair extraction (rotations.py:226-251).
+ * Plain pointers and sizes only; no torch types.  Every entry point returns
+ * an hjb_status; hjb_last_error() returns a message for the calling thread.
+ *
+ * Conventions (as the reference, core.py:1-34): G is column-major, m x n,
+ * leading dimension ldg >= m, float64 or complex128 (interleaved re/im);
+ * signs is an int8 vector of +-1.  Block index / ring rank conventions follow
+ * strategies.py (1-based block indices, nbl = 2p).
+ */
+#ifndef HJB200_H
+#define HJB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HJB_ABI_VERSION 1
+
+typedef enum {
+  HJB_OK = 0,
+  HJB_EINVAL = 1,            /* -> ValueError (parallel.py:55-62, 264-265)          */
+  HJB_PIVOT_INDEFINITE = 2,  /* -> PivotDefinitenessError(r, s) (rotations.py:198)  */
+  HJB_CHOL_FAIL = 3,         /* -> DefinitenessError (blocking.py:106-112)          */
+  HJB_ECUDA = 4,             /* -> RuntimeError                                      */
+  HJB_ENCCL = 5,             /* -> RuntimeError                                      */
+  HJB_ENOMEM = 6             /* -> MemoryError                                       */
+} hjb_status;
+
+typedef enum { HJB_F64 = 0, HJB_C128 = 1 } hjb_dtype;
+typedef enum { HJB_MODULUS = 0, HJB_ROUND_ROBIN = 1 } hjb_strategy;   /* strategies.py:14-16 */
+typedef enum { HJB_HOST = 0, HJB_DEVICE = 1 } hjb_memspace;
+
+typedef struct {
+  int32_t dtype;          /* hjb_dtype */
+  int32_t memspace;       /* where G_in / G_out live */
+  int64_t m, n;           /* rows, columns of G */
+  int64_t ldg;            /* leading dimension of G_in and G_out (>= m) */
+  const void *G_in;       /* input factor (not modified unless G_out == G_in on device) */
+  void *G_out;            /* output factor, same column order as G_in (parallel.py:299-301) */
+  const int8_t *signs;    /* host pointer, n entries of +-1 */
+  int32_t p;              /* ring workers; nbl = 2p uniform blocks (parallel.py:266) */
+  int32_t strategy;       /* hjb_strategy */
+  double orth_tol;        /* <= 0: sqrt(rows of swept factor)*eps (rotations.py:76-77) */
+  double quad_tol;        /* <= 0: cols of swept factor * eps (rotations.py:79-80) */
+  int32_t max_sweeps;     /* outer and inner sweep cap (rotations.py:67) */
+  int32_t device;         /* CUDA device ordinal */
+  void *stream;           /* cudaStream_t to run on; NULL = library stream */
+  void *comm;             /* hjb_comm from hjb_comm_init, or NULL for one GPU */
+  int32_t flags;          /* HJB_FLAG_* */
+} hjb_problem;
+
+#define HJB_FLAG_PHASE_TIMES 1   /* record per-phase device times (adds events) */
+#define HJB_FLAG_NO_GRAPH    2   /* launch kernels directly instead of CUDA graphs */
+
+typedef struct {
+  int32_t sweeps;           /* DiagInfo.sweeps (rotations.py:111) */
+  int32_t converged;        /* DiagInfo.converged */
+  int64_t rotations;        /* DiagInfo.rotations (incl. inner and pre-pass) */
+  int64_t big_rotations;    /* DiagInfo.big_rotations */
+  double max_abs_t;         /* DiagInfo.max_abs_t */
+  int32_t fail_rank;        /* worker rank that raised (parallel.py:296-298), else -1 */
+  int32_t fail_r, fail_s;   /* PivotDefinitenessError(r, s) indices, else -1 */
+  int64_t pairs_visited;    /* pair steps executed (Gram always computed) */
+  int64_t pairs_updated;    /* pair steps whose update ran (parallel.py:203) */
+  int64_t prepass_visited;  /* pre-pass blocks (parallel.py:138-148) */
+  int64_t prepass_updated;  /* pre-pass blocks whose update ran (parallel.py:145) */
+  int64_t fallbacks;        /* dense-Cholesky fallbacks (parallel.py:196-198) */
+  double t_total_ms;        /* device time of the solve (H2D/D2H excluded) */
+  double t_gram_ms, t_pivot_ms, t_update_ms, t_exchange_ms;  /* with HJB_FLAG_PHASE_TIMES */
+  int64_t exchange_bytes;   /* bytes sent over NCCL by this rank */
+  int32_t cluster_size;     /* pivot-kernel cluster size used */
+  int32_t gram_splits;      /* split-K factor of the Gram kernel */
+  int64_t inner_sweeps;     /* sum of inner (pivot-level) sweeps over all pivots */
+  int64_t inner_pair_visits;/* inner 2x2 pivots examined (sweeps * N(N-1)/2 per pivot) */
+} hjb_result;
+
+/* Library / ABI version (HJB_ABI_VERSION). */
+int hjb_version(void);
+/* Message for the last non-OK status on this thread. */
+const char *hjb_last_error(void);
+/* Number of visible CUDA devices (0 without a GPU); never fails. */
+int hjb_device_count(void);
+
+/*
+ * Whole 2F ring solve: replaces parallel_jacobi(G, signs, SolverConfig(
+ * variant="2F", strategy, p, tol=Tolerances(orth_tol, quad_tol, max_sweeps)))
+ * (parallel.py:255-309; solve.py:44-64 dispatches here).  Non-convergence is
+ * not an error: HJB_OK with converged = 0 (parallel.py:307).
+ */
+int hjb_solve(const hjb_problem *prob, hjb_result *res);
+
+/*
+ * Ring schedule, bit-exact with generate_sweep_schedule (strategies.py:143-176)
+ * and the per-worker StepPlans (strategies.py:75-136).  layouts: int32
+ * [steps][p][2] (i_blk, j_blk); plans (may be NULL): int32 [steps][p][4]
+ * (snd_rnk, snd_blk, rcv_rnk, rcv_blk); steps = sweeps * steps_per_sweep.
+ * Host-only; needs no GPU.
+ */
+int hjb_schedule(int32_t strategy, int32_t p, int32_t sweeps, int32_t *layouts,
+                 int32_t *plans);
+/* steps_per_sweep (strategies.py:27-28). */
+int hjb_steps_per_sweep(int32_t strategy, int32_t p);
+
+/*
+ * Eigenpair extraction on device (rotations.py:226-251): lam[k] =
+ * signs[k]*||g_k||^2, U[:,k] = g_k/||g_k||, then U[:, out] = U[:, perm[out]]
+ * if perm != NULL (perm is a device int64 array).  G, U, lam device
+ * pointers; U may alias G only when perm == NULL.  Returns HJB_CHOL_FAIL
+ * (StructuralError) on a zero column.
+ */
+int hjb_extract(int32_t dtype, int64_t m, int64_t n, const void *G, int64_t ldg,
+                const int8_t *signs_dev, double *lam, void *U, int64_t ldu,
+                const int64_t *perm, void *stream);
+
+/* ---- kernel-level entry points (device pointers), used by parity tests ---- */
+
+/*
+ * Batched Gram of column-block pairs: for item t with column offsets
+ * (oi, oj) and widths (ni, nj): A_t = G[:, oi:oi+ni]^H G[:, oj:oj+nj]
+ * (core.py:42-56), D_t[0:ni] = colnorms^2 of the first block and
+ * D_t[bmax:bmax+nj] of the second.  nj == 0 means the diagonal Gram of the
+ * first block (ni x ni, upper triangle meaningful).  items: int32 [count][4].
+ * A: [count][bmax*bmax] column-major ld bmax; D: [count][2*bmax].
+ */
+int hjb_gram(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_t *items_host,
+             int32_t count, int32_t bmax, void *A, double *D, void *stream);
+
+/*
+ * Pivot diagonalisation for a batch of items (parallel.py:193-202 +
+ * blocking.py:115-138 + rotations.py:203-223): builds R by the structured
+ * Cholesky from (D_i, A_ij, D_j) -- or, for nj == 0, R = chol(A) -- then
+ * diagonalises R with the tournament-ordered J-Jacobi and returns the
+ * accumulated W ([count][NMAX*NMAX], ld NMAX where NMAX = 2*bmax rounded to a
+ * supported size) and per-item stats int64/double [count][8]:
+ * (rotations, big, max_t bits, inner sweeps, status, fail_r, fail_s, fallback).
+ * R_out (optional, may be NULL) receives the final R.
+ */
+int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_t *items_host,
+              int32_t count, int32_t bmax, const void *A, const double *D,
+              const int8_t *signs_dev, double orth_tol, double quad_tol, int32_t max_sweeps,
+              void *W, int64_t *stats, void *R_out, int32_t cluster, void *stream);
+
+/* Leading dimension of W / R_out used by hjb_pivot for a given bmax. */
+int hjb_pivot_ld(int32_t bmax);
+
+/*
+ * Block update [G_i G_j] <- [G_i G_j] W for items whose stats[0] > 0
+ * (parallel.py:203-207), in place.  W as produced by hjb_pivot.
+ */
+int hjb_update(int32_t dtype, int64_t m, void *G, int64_t ldg, const int32_t *items_host,
+               int32_t count, int32_t bmax, const void *W, const int64_t *stats,
+               void *stream);
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---- */
+
+/* 128-byte NCCL unique id for rank 0 to broadcast (e.g. via torch.distributed). */
+int hjb_comm_unique_id(char out[128]);
+/* Create the communicator of this rank; *comm receives an opaque handle. */
+int hjb_comm_init(const char id[128], int32_t world, int32_t rank, int32_t device, void **comm);
+int hjb_comm_destroy(void *comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HJB200_H */

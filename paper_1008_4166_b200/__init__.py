@@ -1,0 +1,31 @@
+"""B200-native hot path of the blocked one-sided hyperbolic J-Jacobi
+eigensolver (arXiv 1008.4166), drop-in for the reference package ``hjacobi``'s
+``parallel_jacobi`` / ``run_solver`` / ``solve_hermitian`` entry points with
+variant "2F".  Kernels: libhjb200.so (sm_100a); no CPU fallback.
+"""
+
+from .blocking import BlockPartition, greedy_partition, num_blocks, uniform_partition
+from .core import EigenResult, as_matrix, as_signs
+from .errors import (
+    ChannelTimeoutError,
+    DefinitenessError,
+    HJacobiError,
+    NonConvergenceError,
+    PivotDefinitenessError,
+    RankDeficiencyError,
+    SingularMatrixError,
+    StructuralError,
+)
+from .parallel import SolverConfig, parallel_jacobi
+from .rotations import DiagInfo, Tolerances, extract_eigen
+from .strategies import MODULUS, ROUND_ROBIN, generate_sweep_schedule, normalize_strategy, steps_per_sweep
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BlockPartition", "ChannelTimeoutError", "DefinitenessError", "DiagInfo", "EigenResult",
+    "HJacobiError", "MODULUS", "NonConvergenceError", "PivotDefinitenessError", "ROUND_ROBIN",
+    "RankDeficiencyError", "SingularMatrixError", "SolverConfig", "StructuralError", "Tolerances",
+    "as_matrix", "as_signs", "extract_eigen", "generate_sweep_schedule", "greedy_partition",
+    "normalize_strategy", "num_blocks", "parallel_jacobi", "steps_per_sweep", "uniform_partition",
+]

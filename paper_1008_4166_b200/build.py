@@ -1,0 +1,91 @@
+"""Build libhjb200.so (sm_100a) in-tree with nvcc.
+
+    python -m paper_1008_4166_b200.build [--verbose-ptxas]
+
+Every translation unit is compiled with
+``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` and linked against
+the NCCL that ships with torch (same soname the process already has loaded).
+"""
+
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libhjb200.so")
+OBJ = os.path.join(ROOT, "build", "obj")
+SOURCES = ["schedule.cpp", "gram.cu", "pivot.cu", "update.cu", "solver.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dirs():
+    try:
+        import nvidia.nccl as nn  # torch's NCCL wheel
+        base = list(nn.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    except Exception:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+def nvcc():
+    return shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+
+
+def _compile(src, inc, verbose):
+    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+    flags = [nvcc(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+             "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", src, "-o", obj]
+    if src.endswith(".cu"):
+        flags += ["--expt-relaxed-constexpr"]
+        if verbose:
+            flags += ["-Xptxas", "-v"]
+    else:
+        flags[1:1] = ["-x", "cu"]
+    r = subprocess.run(flags, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    return obj, r.stderr
+
+
+def _stale():
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(ROOT, "include", "hjb200.h"))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force=False, verbose=False):
+    if not force and not _stale():
+        return OUT
+    os.makedirs(OBJ, exist_ok=True)
+    inc, lib = nccl_dirs()
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    with cf.ThreadPoolExecutor(len(srcs)) as ex:
+        results = list(ex.map(lambda s: _compile(s, inc, verbose), srcs))
+    if verbose:
+        for _, log in results:
+            sys.stderr.write(log)
+    objs = [o for o, _ in results]
+    tmp = OUT + ".tmp"
+    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-L", lib, "-l:libnccl.so.2",
+           "-Xlinker", f"-rpath,{lib}", "-lcudart"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose="--verbose-ptxas" in sys.argv))

@@ -1,0 +1,254 @@
+// Batched long-K Gram of block-column pairs on FP64 tensor cores (DMMA).
+//
+// Replaces the per-pair Gram A_ij = G_i^H G_j of the reference's 2F step
+// (pkg/src/hjacobi/parallel.py:193 -> core.py:42-56) and the diagonal-block
+// Gram of the F pre-pass (parallel.py:143), and fuses the column-norm
+// refresh D = colnorms^2 (parallel.py:208-209 / core.py:59-61) into the same
+// pass over the data.
+//
+// Layout: G column-major (ld = ldg); block column = contiguous m x b slab.
+// One CTA computes a TILE x TILE tile of one item's Gram over one K split;
+// operands are staged through shared memory with a cp.async pipeline and fed
+// to mma.sync.m8n8k4.f64 (SASS DMMA).  Split-K partials are reduced by the
+// last-arriving CTA of each tile in fixed split order (deterministic).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hjb {
+
+template <typename T, int WM, int KC, int STAGES>
+struct GramCfg {
+  static constexpr int TILE = 32 * WM;
+  static constexpr int NT = 32 * WM * WM;
+  static constexpr int PAD = S<T>::cx ? 4 : 4;
+  static constexpr int KCP = KC + PAD;                      // elements per staged column
+  static constexpr int STAGE_ELEMS = 2 * TILE * KCP;        // X and Y tiles
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(T);
+};
+
+// (X^H Y) fragment products: real a*b; complex conj(a)*b on 4 DMMAs.
+template <typename T> struct GramAcc;
+template <> struct GramAcc<double> {
+  double v[2];
+  __device__ void zero() { v[0] = v[1] = 0.0; }
+  __device__ void mma(double a, double b) { dmma(v[0], v[1], a, b); }
+  __device__ double get(int q) const { return v[q]; }
+};
+template <> struct GramAcc<cplx> {
+  double r[2], i[2];
+  __device__ void zero() { r[0] = r[1] = i[0] = i[1] = 0.0; }
+  __device__ void mma(cplx a, cplx b) {
+    // conj(a) b = (ar br + ai bi) + i (ar bi - ai br)
+    dmma(r[0], r[1], a.x, b.x);
+    dmma(r[0], r[1], a.y, b.y);
+    dmma(i[0], i[1], a.x, b.y);
+    dmma(i[0], i[1], -a.y, b.x);
+  }
+  __device__ cplx get(int q) const { return make_double2(r[q], i[q]); }
+};
+
+template <typename T, int WM, int KC, int STAGES, int VEC>
+__global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
+    gram_kernel(GramArgs a) {
+  using Cfg = GramCfg<T, WM, KC, STAGES>;
+  constexpr int TILE = Cfg::TILE, NT = Cfg::NT, KCP = Cfg::KCP;
+  constexpr int EPP = VEC / int(sizeof(T));       // elements per cp.async piece
+  constexpr int PPC = KC / EPP;                   // pieces per staged column
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *smem = reinterpret_cast<T *>(smem_raw);
+  __shared__ int s_last;
+
+  const int tiles = a.tiles;
+  const int ti = blockIdx.x / tiles, tj = blockIdx.x % tiles;
+  const int split = blockIdx.y;
+  const int item_id = blockIdx.z;
+  const Item it = a.items[item_id];
+  const bool dense = it.nj == 0;
+  const int nX = it.ni, nY = dense ? it.ni : it.nj;
+  const int oX = it.oi + ti * TILE, oY = (dense ? it.oi : it.oj) + tj * TILE;
+  const int cX = min(TILE, nX - ti * TILE), cY = min(TILE, nY - tj * TILE);  // may be <= 0
+  const int64_t k0 = int64_t(split) * a.ksplit;
+  const int64_t k1 = min(a.m, k0 + a.ksplit);
+  const int nchunks = k1 > k0 ? int((k1 - k0 + KC - 1) / KC) : 0;
+  const T *G = reinterpret_cast<const T *>(a.G);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WM, wn = warp % WM;
+
+  auto load_stage = [&](int stage, int chunk) {
+    T *Xs = smem + stage * Cfg::STAGE_ELEMS;
+    T *Ys = Xs + TILE * KCP;
+    const int64_t kb = k0 + int64_t(chunk) * KC;
+    for (int pc = tid; pc < 2 * TILE * PPC; pc += NT) {
+      const int which = pc / (TILE * PPC);
+      const int rem = pc % (TILE * PPC);
+      const int col = rem / PPC, within = rem % PPC;
+      const int64_t row = kb + within * EPP;
+      const int ccount = which ? cY : cX;
+      const int coff = which ? oY : oX;
+      int64_t valid = (col < ccount) ? min(int64_t(EPP), k1 - row) : 0;
+      if (valid < 0) valid = 0;
+      const T *src = valid > 0 ? G + int64_t(coff + col) * a.ldg + row : G;
+      T *dst = (which ? Ys : Xs) + col * KCP + within * EPP;
+      if (VEC == 16)
+        cp_async16(dst, src, int(valid * sizeof(T)));
+      else
+        cp_async8(dst, src, int(valid * sizeof(T)));
+    }
+  };
+
+  GramAcc<T> acc[4][4];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni].zero();
+  double dx[4] = {0, 0, 0, 0}, dy[4] = {0, 0, 0, 0};
+  const bool do_dx = !dense && tj == 0 && wn == 0;
+  const bool do_dy = !dense && ti == 0 && wm == 0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nchunks) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = c + STAGES - 1;
+      if (nxt < nchunks) load_stage(nxt % STAGES, nxt);
+      cp_async_commit();
+    }
+    const T *Xs = smem + (c % STAGES) * Cfg::STAGE_ELEMS;
+    const T *Ys = Xs + TILE * KCP;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      T fa[4], fb[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+        fa[mi] = Xs[(wm * 32 + mi * 8 + (lane >> 2)) * KCP + kk + (lane & 3)];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+        fb[ni] = Ys[(wn * 32 + ni * 8 + (lane >> 2)) * KCP + kk + (lane & 3)];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) acc[mi][ni].mma(fa[mi], fb[ni]);
+      if (do_dx) {
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) dx[mi] += abs2(fa[mi]);
+      }
+      if (do_dy) {
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dy[ni] += abs2(fb[ni]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---- write this split's partial (or the final value when unsplit) ----
+  const int bmax = a.bmax;
+  const int64_t asz = int64_t(bmax) * bmax;
+  T *Aout = reinterpret_cast<T *>(a.splits > 1 ? a.Apart : a.A) +
+            (a.splits > 1 ? (int64_t(item_id) * a.splits + split) * asz : int64_t(item_id) * asz);
+  double *Dout = a.splits > 1 ? a.Dpart + (int64_t(item_id) * a.splits + split) * 2 * bmax
+                              : a.D + int64_t(item_id) * 2 * bmax;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = ti * TILE + wm * 32 + mi * 8 + (lane >> 2);
+        const int cc = tj * TILE + wn * 32 + ni * 8 + 2 * (lane & 3) + q;
+        if (r < bmax && cc < bmax) Aout[r + int64_t(cc) * bmax] = acc[mi][ni].get(q);
+      }
+  // column norms: reduce the 4 lanes holding the same column
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    dx[mi] += __shfl_xor_sync(0xffffffffu, dx[mi], 1);
+    dx[mi] += __shfl_xor_sync(0xffffffffu, dx[mi], 2);
+    dy[mi] += __shfl_xor_sync(0xffffffffu, dy[mi], 1);
+    dy[mi] += __shfl_xor_sync(0xffffffffu, dy[mi], 2);
+  }
+  if ((lane & 3) == 0) {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int r = ti * TILE + wm * 32 + mi * 8 + (lane >> 2);
+      if (do_dx && r < bmax) Dout[r] = dx[mi];
+      const int cc = tj * TILE + wn * 32 + mi * 8 + (lane >> 2);
+      if (do_dy && cc < bmax) Dout[bmax + cc] = dy[mi];
+    }
+  }
+  if (a.splits == 1) return;
+
+  // ---- deterministic split-K reduction by the last CTA of this tile ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned *tk = a.tickets + int64_t(item_id) * tiles * tiles + blockIdx.x;
+    const unsigned prev = atomicAdd(tk, 1u);
+    s_last = (prev == unsigned(a.splits - 1));
+    if (s_last) *tk = 0u;  // re-arm for the next launch
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const T *Ap = reinterpret_cast<const T *>(a.Apart) + int64_t(item_id) * a.splits * asz;
+  T *Af = reinterpret_cast<T *>(a.A) + int64_t(item_id) * asz;
+  for (int e = tid; e < TILE * TILE; e += NT) {
+    const int r = ti * TILE + (e % TILE), cc = tj * TILE + (e / TILE);
+    if (r >= bmax || cc >= bmax) continue;
+    const int64_t off = r + int64_t(cc) * bmax;
+    T s = __ldcg(Ap + off);
+    for (int sp = 1; sp < a.splits; ++sp) s = add(s, __ldcg(Ap + sp * asz + off));
+    Af[off] = s;
+  }
+  if (!dense) {
+    const double *Dp = a.Dpart + int64_t(item_id) * a.splits * 2 * bmax;
+    double *Df = a.D + int64_t(item_id) * 2 * bmax;
+    for (int e = tid; e < 2 * TILE; e += NT) {
+      const bool y = e >= TILE;
+      const int idx = (y ? tj : ti) * TILE + (e % TILE);
+      if ((y ? ti != 0 : tj != 0) || idx >= bmax) continue;
+      const int off = (y ? bmax : 0) + idx;
+      double s = __ldcg(Dp + off);
+      for (int sp = 1; sp < a.splits; ++sp) s += __ldcg(Dp + int64_t(sp) * 2 * bmax + off);
+      Df[off] = s;
+    }
+  }
+}
+
+template <typename T, int WM, int KC, int STAGES, int VEC>
+static cudaError_t launch_gram_t(const GramArgs &a, cudaStream_t st) {
+  using Cfg = GramCfg<T, WM, KC, STAGES>;
+  auto k = gram_kernel<T, WM, KC, STAGES, VEC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(a.tiles * a.tiles, a.splits, a.count);
+  k<<<grid, Cfg::NT, Cfg::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+int gram_tile(int bmax) { return bmax <= 32 ? 32 : 64; }
+
+cudaError_t launch_gram(bool cx, GramArgs a, cudaStream_t st) {
+  const int tile = gram_tile(a.bmax);
+  a.tiles = (a.bmax + tile - 1) / tile;
+  const bool v16 = cx || (a.ldg % 2 == 0);
+  if (cx) {
+    if (tile == 32) return launch_gram_t<cplx, 1, 16, 3, 16>(a, st);
+    return launch_gram_t<cplx, 2, 16, 3, 16>(a, st);
+  }
+  if (tile == 32)
+    return v16 ? launch_gram_t<double, 1, 32, 3, 16>(a, st) : launch_gram_t<double, 1, 32, 3, 8>(a, st);
+  return v16 ? launch_gram_t<double, 2, 32, 3, 16>(a, st) : launch_gram_t<double, 2, 32, 3, 8>(a, st);
+}
+
+int gram_kc(bool cx) { return cx ? 16 : 32; }
+
+}  // namespace hjb

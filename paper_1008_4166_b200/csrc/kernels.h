@@ -1,0 +1,65 @@
+// Launch interfaces of the hjb200 kernels (host side).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace hjb {
+
+struct GramArgs {
+  const void *G;
+  int64_t ldg, m;
+  const Item *items;
+  int count;
+  int bmax;
+  int tiles;        // tiles per dimension (set by launch_gram)
+  int splits;       // split-K factor
+  int64_t ksplit;   // rows per split (multiple of the K chunk)
+  void *Apart;      // [count][splits][bmax*bmax] partials (splits > 1)
+  double *Dpart;    // [count][splits][2*bmax]
+  void *A;          // [count][bmax*bmax] final Gram, column-major ld bmax
+  double *D;        // [count][2*bmax] final column norms^2
+  unsigned *tickets;  // [count][tiles*tiles], zero-initialised
+};
+cudaError_t launch_gram(bool cx, GramArgs a, cudaStream_t st);
+int gram_tile(int bmax);
+int gram_kc(bool cx);
+
+struct PivotArgs {
+  const void *G;
+  int64_t ldg, m;
+  const Item *items;
+  int count;
+  int bmax;
+  void *A;            // [count][bmax*bmax] Gram (overwritten with R_ij)
+  const double *D;    // [count][2*bmax]
+  const int8_t *signs;
+  double orth_tol, quad_tol;  // <= 0: defaults of rotations.py:76-80
+  int max_sweeps;
+  void *W;            // [count][nmax*nmax] accumulated transformation
+  int64_t *stats;     // [count][ST_N]
+  void *Rout;         // optional [count][nmax*nmax]
+  int nmax;
+};
+// cluster: 0 = automatic choice
+cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used);
+int pivot_nmax(int bmax);   // NMAX instance for a block width
+int pivot_default_cluster(bool cx, int nmax);
+
+struct UpdateArgs {
+  void *G;
+  int64_t ldg, m;
+  const Item *items;
+  int count;
+  int nmax;
+  const void *W;
+  const int64_t *stats;
+};
+cudaError_t launch_update(bool cx, const UpdateArgs &a, cudaStream_t st);
+
+cudaError_t launch_extract(bool cx, int64_t m, int64_t n, const void *G, int64_t ldg,
+                           const int8_t *signs, double *lam, void *U, int64_t ldu,
+                           const int64_t *perm, int *zero_flag, cudaStream_t st);
+
+}  // namespace hjb

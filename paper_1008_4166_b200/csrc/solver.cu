@@ -1,0 +1,694 @@
+// Host driver and C ABI of hjb200 (include/hjb200.h).
+//
+// hjb_solve replaces the reference's parallel_jacobi (pkg/src/hjacobi/
+// parallel.py:255-309) for variant 2F.  The P ring workers become the CTA
+// clusters of one batched launch per phase; the ring exchange of the
+// reference (parallel.py:212-221) is an index remap on one GPU (every block
+// keeps its column position in the device copy of G) and an NCCL send/recv of
+// the blocks that cross a GPU boundary with several GPUs.  Per sweep:
+//   pre-pass: Gram(diag) -> pivot(dense) -> update        (parallel.py:138-148)
+//   steps:    Gram(pair) -> pivot(structured) -> update   (parallel.py:185-210)
+//             [-> NCCL block exchange]                     (parallel.py:212-221)
+//   one host read of the per-item counters, all-reduced over GPUs
+//                                                          (parallel.py:239-244)
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hjb200.h"
+#include "kernels.h"
+#include "schedule.h"
+
+using namespace hjb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(HJB_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+#define NK(x)                                                                           \
+  do {                                                                                  \
+    ncclResult_t r_ = (x);                                                              \
+    if (r_ != ncclSuccess)                                                              \
+      return fail(HJB_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_));          \
+  } while (0)
+
+// grow-only device buffer
+struct DBuf {
+  void *p = nullptr;
+  size_t n = 0;
+  int dev = -1;
+  cudaError_t reserve(size_t bytes) {
+    if (bytes <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+    if (e == cudaSuccess) n = std::max<size_t>(bytes, 256);
+    return e;
+  }
+};
+
+struct HBuf {
+  void *p = nullptr;
+  size_t n = 0;
+  cudaError_t reserve(size_t bytes) {
+    if (bytes <= n && p) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMallocHost(&p, std::max<size_t>(bytes, 256));
+    if (e == cudaSuccess) n = std::max<size_t>(bytes, 256);
+    return e;
+  }
+};
+
+struct Workspace {
+  DBuf G, items, A, Apart, D, Dpart, tickets, W, stats, signs, red, lam, flag;
+  HBuf stats_h, red_h;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> events;
+};
+
+std::mutex g_mu;
+Workspace g_ws[64];
+
+struct Comm {
+  ncclComm_t nccl = nullptr;
+  int world = 1, rank = 0, device = 0;
+};
+
+size_t esz(int dtype) { return dtype == HJB_C128 ? 16 : 8; }
+
+struct Partition {
+  std::vector<int> off, width;  // per block (0-based block index)
+  int bmax = 0;
+};
+
+Partition uniform_partition(int64_t n, int nbl) {  // blocking.py:63-68
+  Partition P;
+  const int64_t q = n / nbl, r = n % nbl;
+  int64_t o = 0;
+  for (int b = 0; b < nbl; ++b) {
+    const int w = int(q + (b < r ? 1 : 0));
+    P.off.push_back(int(o));
+    P.width.push_back(w);
+    P.bmax = std::max(P.bmax, w);
+    o += w;
+  }
+  return P;
+}
+
+int gram_splits(int count, int tiles, int64_t m, int kc, int64_t *ksplit) {
+  const int64_t chunks = (m + kc - 1) / kc;
+  const int64_t target = 2 * 148;
+  int64_t s = (target + int64_t(count) * tiles * tiles - 1) / (int64_t(count) * tiles * tiles);
+  s = std::max<int64_t>(1, std::min(s, chunks));
+  const int64_t cps = (chunks + s - 1) / s;  // chunks per split
+  *ksplit = cps * kc;
+  return int((m + *ksplit - 1) / *ksplit);
+}
+
+struct PhaseCtx {
+  bool cx;
+  int64_t m, ld;
+  void *G;
+  int bmax, nmax, cluster;
+  const int8_t *signs;
+  double otol, qtol;
+  int max_sweeps;
+  Workspace *ws;
+  cudaStream_t st;
+  int splits_used = 0;
+};
+
+// Gram -> pivot -> update for one batch of items (device item table).
+int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, void *Rout,
+              cudaEvent_t *ev) {
+  if (count == 0) return HJB_OK;
+  const int tile = gram_tile(c.bmax);
+  const int tiles = (c.bmax + tile - 1) / tile;
+  int64_t ksplit = 0;
+  const int splits = gram_splits(count, tiles, c.m, gram_kc(c.cx), &ksplit);
+  c.splits_used = splits;
+  GramArgs g{};
+  g.G = c.G;
+  g.ldg = c.ld;
+  g.m = c.m;
+  g.items = items_d;
+  g.count = count;
+  g.bmax = c.bmax;
+  g.splits = splits;
+  g.ksplit = ksplit;
+  g.Apart = c.ws->Apart.p;
+  g.Dpart = static_cast<double *>(c.ws->Dpart.p);
+  g.A = c.ws->A.p;
+  g.D = static_cast<double *>(c.ws->D.p);
+  g.tickets = static_cast<unsigned *>(c.ws->tickets.p);
+  if (ev) CK(cudaEventRecord(ev[0], c.st));
+  CK(launch_gram(c.cx, g, c.st));
+  if (ev) CK(cudaEventRecord(ev[1], c.st));
+  PivotArgs pa{};
+  pa.G = c.G;
+  pa.ldg = c.ld;
+  pa.m = c.m;
+  pa.items = items_d;
+  pa.count = count;
+  pa.bmax = c.bmax;
+  pa.A = c.ws->A.p;
+  pa.D = static_cast<double *>(c.ws->D.p);
+  pa.signs = c.signs;
+  pa.orth_tol = c.otol;
+  pa.quad_tol = c.qtol;
+  pa.max_sweeps = c.max_sweeps;
+  pa.W = c.ws->W.p;
+  pa.stats = stats_d;
+  pa.Rout = Rout;
+  pa.nmax = c.nmax;
+  int used = 0;
+  CK(launch_pivot(c.cx, pa, c.cluster, c.st, &used));
+  c.cluster = used;
+  if (ev) CK(cudaEventRecord(ev[2], c.st));
+  UpdateArgs u{};
+  u.G = c.G;
+  u.ldg = c.ld;
+  u.m = c.m;
+  u.items = items_d;
+  u.count = count;
+  u.nmax = c.nmax;
+  u.W = c.ws->W.p;
+  u.stats = stats_d;
+  CK(launch_update(c.cx, u, c.st));
+  if (ev) CK(cudaEventRecord(ev[3], c.st));
+  return HJB_OK;
+}
+
+int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_count, int64_t m) {
+  const size_t w = cx ? 16 : 8;
+  const int tile = gram_tile(bmax);
+  const int tiles = (bmax + tile - 1) / tile;
+  int64_t ks = 0;
+  int max_splits = 1;
+  for (int cnt = 1; cnt <= max_count; cnt = cnt < max_count ? std::min(max_count, cnt * 2) : cnt + 1)
+    max_splits = std::max(max_splits, gram_splits(cnt, tiles, m, gram_kc(cx), &ks));
+  CK(ws.A.reserve(size_t(max_count) * bmax * bmax * w));
+  CK(ws.Apart.reserve(size_t(max_count) * max_splits * bmax * bmax * w));
+  CK(ws.D.reserve(size_t(max_count) * 2 * bmax * 8));
+  CK(ws.Dpart.reserve(size_t(max_count) * max_splits * 2 * bmax * 8));
+  const size_t tk = size_t(max_count) * tiles * tiles * sizeof(unsigned);
+  if (ws.tickets.n < tk) {
+    CK(ws.tickets.reserve(tk));
+    CK(cudaMemset(ws.tickets.p, 0, ws.tickets.n));
+  }
+  CK(ws.W.reserve(size_t(max_count) * nmax * nmax * w));
+  return HJB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hjb_version(void) { return HJB_ABI_VERSION; }
+const char *hjb_last_error(void) { return g_err.c_str(); }
+int hjb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int hjb_steps_per_sweep(int32_t strategy, int32_t p) {
+  if (p < 1 || (strategy != HJB_MODULUS && strategy != HJB_ROUND_ROBIN)) return -1;
+  return strategy == HJB_MODULUS ? 2 * p : 2 * p - 1;
+}
+
+int hjb_schedule(int32_t strategy, int32_t p, int32_t sweeps, int32_t *layouts, int32_t *plans) {
+  if (p < 1 || sweeps < 0 || (strategy != HJB_MODULUS && strategy != HJB_ROUND_ROBIN) || !layouts)
+    return fail(HJB_EINVAL, "hjb_schedule: invalid argument");
+  try {
+    RingSchedule rs(strategy, p);
+    int64_t step = 0;
+    for (int sw = 1; sw <= sweeps; ++sw) {
+      for (int s = 0; s < rs.steps_per_sweep(); ++s, ++step) {
+        for (int q = 0; q < p; ++q) {
+          layouts[(step * p + q) * 2 + 0] = rs.i_blk(q);
+          layouts[(step * p + q) * 2 + 1] = rs.j_blk(q);
+        }
+        std::vector<StepPlan> pl = rs.advance(sw);
+        if (plans)
+          for (int q = 0; q < p; ++q) {
+            int32_t *o = plans + (step * p + q) * 4;
+            o[0] = pl[q].snd_rnk;
+            o[1] = pl[q].snd_blk;
+            o[2] = pl[q].rcv_rnk;
+            o[3] = pl[q].rcv_blk;
+          }
+      }
+    }
+  } catch (const std::exception &e) {
+    return fail(HJB_EINVAL, e.what());
+  }
+  return HJB_OK;
+}
+
+int hjb_comm_unique_id(char out[128]) {
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "nccl unique id size");
+  std::memcpy(out, &id, 128);
+  return HJB_OK;
+}
+
+int hjb_comm_init(const char id[128], int32_t world, int32_t rank, int32_t device, void **comm) {
+  if (!comm || world < 1 || rank < 0 || rank >= world) return fail(HJB_EINVAL, "hjb_comm_init: bad rank/world");
+  CK(cudaSetDevice(device));
+  Comm *c = new Comm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  ncclResult_t r = ncclCommInitRank(&c->nccl, world, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(HJB_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  *comm = c;
+  return HJB_OK;
+}
+
+int hjb_comm_destroy(void *comm) {
+  if (!comm) return HJB_OK;
+  Comm *c = static_cast<Comm *>(comm);
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+  return HJB_OK;
+}
+
+int hjb_pivot_ld(int32_t bmax) { return pivot_nmax(bmax); }
+
+int hjb_solve(const hjb_problem *pr, hjb_result *res) {
+  if (!pr || !res) return fail(HJB_EINVAL, "null problem/result");
+  std::memset(res, 0, sizeof(*res));
+  res->fail_rank = res->fail_r = res->fail_s = -1;
+  const bool cx = pr->dtype == HJB_C128;
+  if (pr->dtype != HJB_F64 && pr->dtype != HJB_C128) return fail(HJB_EINVAL, "dtype must be float64 or complex128");
+  const int64_t m = pr->m, n = pr->n;
+  if (m < 1 || n < 1 || pr->ldg < m) return fail(HJB_EINVAL, "bad shape / leading dimension");
+  if (pr->p < 1) return fail(HJB_EINVAL, "p must be >= 1");
+  const int P = pr->p, nbl = 2 * P;
+  if (nbl > n) return fail(HJB_EINVAL, "need at least " + std::to_string(nbl) + " columns for p=" + std::to_string(P) + " workers");
+  if (pr->strategy != HJB_MODULUS && pr->strategy != HJB_ROUND_ROBIN) return fail(HJB_EINVAL, "unknown strategy");
+  if (pr->max_sweeps < 1) return fail(HJB_EINVAL, "max_sweeps must be >= 1");
+  if (!pr->signs || !pr->G_in || !pr->G_out) return fail(HJB_EINVAL, "null G/signs pointer");
+  for (int64_t k = 0; k < n; ++k)
+    if (pr->signs[k] != 1 && pr->signs[k] != -1) return fail(HJB_EINVAL, "sign vector entries must be -1 or +1");
+  const Partition part = uniform_partition(n, nbl);
+  const int bmax = part.bmax;
+  const int nmax = pivot_nmax(bmax);
+  if (nmax < 0) return fail(HJB_EINVAL, "block width " + std::to_string(bmax) + " > 128 is not supported (raise p)");
+  Comm *comm = static_cast<Comm *>(pr->comm);
+  const int world = comm ? comm->world : 1, grank = comm ? comm->rank : 0;
+  if (P < world) return fail(HJB_EINVAL, "p must be >= the number of GPUs");
+
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (pr->device < 0 || pr->device >= 64) return fail(HJB_EINVAL, "bad device");
+  CK(cudaSetDevice(pr->device));
+  Workspace &ws = g_ws[pr->device];
+  if (!ws.stream) CK(cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking));
+  cudaStream_t st = pr->stream ? static_cast<cudaStream_t>(pr->stream) : ws.stream;
+  const size_t w = esz(pr->dtype);
+
+  // ---- working copy of G (column positions never change) ----
+  void *Gd = nullptr;
+  int64_t ld = pr->ldg;
+  const bool dev_io = pr->memspace == HJB_DEVICE;
+  if (dev_io) {
+    Gd = pr->G_out;
+    if (pr->G_out != pr->G_in)
+      CK(cudaMemcpy2DAsync(pr->G_out, ld * w, pr->G_in, ld * w, m * w, n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    ld = cx ? m : m + (m & 1);  // even ld keeps 16-byte cp.async alignment
+    CK(ws.G.reserve(size_t(ld) * n * w));
+    Gd = ws.G.p;
+    CK(cudaMemcpy2DAsync(Gd, ld * w, pr->G_in, pr->ldg * w, m * w, n, cudaMemcpyHostToDevice, st));
+  }
+  CK(ws.signs.reserve(n));
+  CK(cudaMemcpyAsync(ws.signs.p, pr->signs, n, cudaMemcpyHostToDevice, st));
+
+  // ---- schedule -> per-sweep item tables of this GPU's workers ----
+  RingSchedule ring(pr->strategy, P);
+  const int steps = ring.steps_per_sweep();
+  auto wlo = [&](int g) { return int((int64_t(g) * P) / world); };
+  auto gpu_of = [&](int q) {
+    int g = int((int64_t(q) * world) / P);
+    while (g + 1 < world && wlo(g + 1) <= q) ++g;
+    while (g > 0 && wlo(g) > q) --g;
+    return g;
+  };
+  const int q_lo = wlo(grank), q_hi = wlo(grank + 1), nloc = q_hi - q_lo;
+  // layouts for max_sweeps sweeps: [sweep][1 + steps][nloc or 2*nloc]
+  const int per_sweep_items = 2 * nloc + steps * nloc;
+  std::vector<Item> items(size_t(pr->max_sweeps) * per_sweep_items);
+  struct Xfer { int blk, peer; bool send; };
+  std::vector<std::vector<Xfer>> xfers(size_t(pr->max_sweeps) * steps);
+  try {
+    for (int sw = 1; sw <= pr->max_sweeps; ++sw) {
+      Item *base = items.data() + size_t(sw - 1) * per_sweep_items;
+      for (int q = q_lo; q < q_hi; ++q) {  // pre-pass: the two blocks each worker holds
+        const int bi = ring.i_blk(q) - 1, bj = ring.j_blk(q) - 1;
+        base[2 * (q - q_lo) + 0] = Item{part.off[bi], part.width[bi], 0, 0};
+        base[2 * (q - q_lo) + 1] = Item{part.off[bj], part.width[bj], 0, 0};
+      }
+      for (int s = 0; s < steps; ++s) {
+        Item *row = base + 2 * nloc + s * nloc;
+        for (int q = q_lo; q < q_hi; ++q) {
+          const int bi = ring.i_blk(q) - 1, bj = ring.j_blk(q) - 1;
+          row[q - q_lo] = Item{part.off[bi], part.width[bi], part.off[bj], part.width[bj]};
+        }
+        std::vector<StepPlan> pl = ring.advance(sw);
+        auto &xf = xfers[size_t(sw - 1) * steps + s];
+        for (int q = q_lo; q < q_hi; ++q) {
+          const int gs = gpu_of(pl[q].snd_rnk), gr = gpu_of(pl[q].rcv_rnk);
+          if (gs != grank) xf.push_back(Xfer{pl[q].snd_blk - 1, gs, true});
+          if (gr != grank) xf.push_back(Xfer{pl[q].rcv_blk - 1, gr, false});
+        }
+      }
+    }
+  } catch (const std::exception &e) {
+    return fail(HJB_EINVAL, e.what());
+  }
+  CK(ws.items.reserve(items.size() * sizeof(Item)));
+  CK(cudaMemcpyAsync(ws.items.p, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice, st));
+  const int max_count = std::max(2 * nloc, 1);
+  if (int rc = reserve_phase_buffers(ws, cx, bmax, nmax, max_count, m)) return rc;
+  const size_t stats_per_sweep = size_t(per_sweep_items) * ST_N;
+  CK(ws.stats.reserve(2 * stats_per_sweep * sizeof(int64_t)));
+  CK(ws.stats_h.reserve(stats_per_sweep * sizeof(int64_t)));
+  CK(ws.red.reserve(4 * sizeof(int64_t)));
+  CK(ws.red_h.reserve(4 * sizeof(int64_t)));
+
+  const bool phase_times = pr->flags & HJB_FLAG_PHASE_TIMES;
+  const int nev = phase_times ? 4 * (1 + steps) + 2 * steps : 0;
+  while (int(ws.events.size()) < nev + 2) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ws.events.push_back(e);
+  }
+  cudaEvent_t ev_start = ws.events[0], ev_stop = ws.events[1];
+  CK(cudaEventRecord(ev_start, st));
+
+  PhaseCtx ctx{};
+  ctx.cx = cx;
+  ctx.m = m;
+  ctx.ld = ld;
+  ctx.G = Gd;
+  ctx.bmax = bmax;
+  ctx.nmax = nmax;
+  ctx.cluster = 0;
+  ctx.signs = static_cast<const int8_t *>(ws.signs.p);
+  ctx.otol = pr->orth_tol;
+  ctx.qtol = pr->quad_tol;
+  ctx.max_sweeps = pr->max_sweeps;
+  ctx.ws = &ws;
+  ctx.st = st;
+  std::vector<int64_t> hstats(stats_per_sweep);
+  double tg = 0, tp = 0, tu = 0, tx = 0;
+
+  for (int sw = 1; sw <= pr->max_sweeps; ++sw) {
+    const Item *it_d = static_cast<const Item *>(ws.items.p) + size_t(sw - 1) * per_sweep_items;
+    int64_t *stats_d = static_cast<int64_t *>(ws.stats.p) + size_t((sw - 1) & 1) * stats_per_sweep;
+    cudaEvent_t *ev = phase_times ? &ws.events[2] : nullptr;
+    if (int rc = run_phase(ctx, it_d, 2 * nloc, stats_d, nullptr, ev)) return rc;
+    for (int s = 0; s < steps; ++s) {
+      cudaEvent_t *evs = phase_times ? &ws.events[2 + 4 * (1 + s)] : nullptr;
+      if (int rc = run_phase(ctx, it_d + 2 * nloc + s * nloc, nloc,
+                             stats_d + size_t(2 * nloc + s * nloc) * ST_N, nullptr, evs))
+        return rc;
+      const auto &xf = xfers[size_t(sw - 1) * steps + s];
+      if (!xf.empty()) {
+        if (phase_times) CK(cudaEventRecord(ws.events[2 + 4 * (1 + steps) + 2 * s], st));
+        NK(ncclGroupStart());
+        for (const Xfer &x : xf) {
+          char *ptr = static_cast<char *>(Gd) + size_t(part.off[x.blk]) * ld * w;
+          const size_t bytes = size_t(part.width[x.blk]) * ld * w;
+          if (x.send) {
+            NK(ncclSend(ptr, bytes, ncclChar, x.peer, comm->nccl, st));
+            res->exchange_bytes += int64_t(bytes);
+          } else {
+            NK(ncclRecv(ptr, bytes, ncclChar, x.peer, comm->nccl, st));
+          }
+        }
+        NK(ncclGroupEnd());
+        if (phase_times) CK(cudaEventRecord(ws.events[2 + 4 * (1 + steps) + 2 * s + 1], st));
+      }
+    }
+    // ---- per-sweep counters (parallel.py:239-244) ----
+    CK(cudaMemcpyAsync(ws.stats_h.p, stats_d, stats_per_sweep * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(hstats.data(), ws.stats_h.p, stats_per_sweep * sizeof(int64_t));
+    int64_t rot = 0;
+    int err = HJB_OK;
+    for (int t = 0; t < per_sweep_items; ++t) {
+      const int64_t *sv = hstats.data() + size_t(t) * ST_N;
+      const bool pre = t < 2 * nloc;
+      const Item &itm = items[size_t(sw - 1) * per_sweep_items + t];
+      const int64_t Nq = itm.ni + itm.nj;
+      res->inner_sweeps += sv[ST_SWEEPS];
+      res->inner_pair_visits += sv[ST_SWEEPS] * (Nq * (Nq - 1) / 2);
+      rot += sv[ST_NROT];
+      res->rotations += sv[ST_NROT];
+      res->big_rotations += sv[ST_NBIG];
+      double mt;
+      std::memcpy(&mt, &sv[ST_MAXT], 8);
+      res->max_abs_t = std::max(res->max_abs_t, mt);
+      res->fallbacks += sv[ST_FALLBACK];
+      if (pre) {
+        res->prepass_visited += 1;
+        res->prepass_updated += sv[ST_NROT] > 0;
+      } else {
+        res->pairs_visited += 1;
+        res->pairs_updated += sv[ST_NROT] > 0;
+      }
+      if (sv[ST_STATUS] != PV_OK && err == HJB_OK) {
+        const int q = q_lo + (pre ? t / 2 : (t - 2 * nloc) % std::max(nloc, 1));
+        res->fail_rank = q;
+        if (sv[ST_STATUS] == PV_INDEFINITE) {
+          err = HJB_PIVOT_INDEFINITE;
+          res->fail_r = int32_t(sv[ST_FR]);
+          res->fail_s = int32_t(sv[ST_FS]);
+        } else {
+          err = HJB_CHOL_FAIL;
+        }
+      }
+    }
+    if (phase_times) {
+      float ms = 0;
+      for (int s = 0; s < 1 + steps; ++s) {
+        cudaEvent_t *e = &ws.events[2 + 4 * s];
+        if (s > 0 && nloc == 0) continue;
+        CK(cudaEventElapsedTime(&ms, e[0], e[1])); tg += ms;
+        CK(cudaEventElapsedTime(&ms, e[1], e[2])); tp += ms;
+        CK(cudaEventElapsedTime(&ms, e[2], e[3])); tu += ms;
+      }
+      for (int s = 0; s < steps; ++s)
+        if (!xfers[size_t(sw - 1) * steps + s].empty()) {
+          CK(cudaEventElapsedTime(&ms, ws.events[2 + 4 * (1 + steps) + 2 * s],
+                                  ws.events[2 + 4 * (1 + steps) + 2 * s + 1]));
+          tx += ms;
+        }
+    }
+    if (world > 1) {  // all-reduce of the sweep's rotation count and error (parallel.py:99-118)
+      int64_t *rh = static_cast<int64_t *>(ws.red_h.p);
+      rh[0] = rot;
+      rh[1] = err != HJB_OK ? 1 : 0;
+      CK(cudaMemcpyAsync(ws.red.p, rh, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      NK(ncclAllReduce(ws.red.p, ws.red.p, 2, ncclInt64, ncclSum, comm->nccl, st));
+      CK(cudaMemcpyAsync(rh, ws.red.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      rot = rh[0];
+      if (rh[1] && err == HJB_OK) err = HJB_CHOL_FAIL;  // another GPU failed
+    }
+    res->sweeps = sw;
+    if (err != HJB_OK) {
+      res->cluster_size = ctx.cluster;
+      return fail(err, err == HJB_PIVOT_INDEFINITE
+                           ? "worker " + std::to_string(res->fail_rank) + ": pivot (" + std::to_string(res->fail_r) +
+                                 ", " + std::to_string(res->fail_s) + ") is not positive definite"
+                           : "worker " + std::to_string(res->fail_rank) + ": matrix is not positive definite");
+    }
+    if (rot == 0) {
+      res->converged = 1;
+      break;
+    }
+  }
+
+  // ---- gather: every block from the GPU whose worker holds it ----
+  if (world > 1) {
+    std::vector<int> owner(nbl, 0);
+    for (int q = 0; q < P; ++q) {
+      owner[ring.i_blk(q) - 1] = gpu_of(q);
+      owner[ring.j_blk(q) - 1] = gpu_of(q);
+    }
+    NK(ncclGroupStart());
+    for (int b = 0; b < nbl; ++b) {
+      char *ptr = static_cast<char *>(Gd) + size_t(part.off[b]) * ld * w;
+      NK(ncclBroadcast(ptr, ptr, size_t(part.width[b]) * ld * w, ncclChar, owner[b], comm->nccl, st));
+    }
+    NK(ncclGroupEnd());
+  }
+  CK(cudaEventRecord(ev_stop, st));
+  if (!dev_io)
+    CK(cudaMemcpy2DAsync(pr->G_out, pr->ldg * w, Gd, ld * w, m * w, n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float tot = 0;
+  CK(cudaEventElapsedTime(&tot, ev_start, ev_stop));
+  res->t_total_ms = tot;
+  res->t_gram_ms = tg;
+  res->t_pivot_ms = tp;
+  res->t_update_ms = tu;
+  res->t_exchange_ms = tx;
+  res->cluster_size = ctx.cluster;
+  res->gram_splits = ctx.splits_used;
+  return HJB_OK;
+}
+
+// ---------------------------------------------------------------- kernel-level entry points
+
+static int upload_items(Workspace &ws, const int32_t *items_host, int count, cudaStream_t st) {
+  CK(ws.items.reserve(size_t(count) * sizeof(Item)));
+  CK(cudaMemcpyAsync(ws.items.p, items_host, size_t(count) * sizeof(Item), cudaMemcpyHostToDevice, st));
+  return HJB_OK;
+}
+
+int hjb_gram(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_t *items_host, int32_t count,
+             int32_t bmax, void *A, double *D, void *stream) {
+  if (count < 1 || bmax < 1 || m < 1 || !G || !A || !D) return fail(HJB_EINVAL, "hjb_gram: bad arguments");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  Workspace &ws = g_ws[dev];
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = upload_items(ws, items_host, count, st)) return rc;
+  const bool cx = dtype == HJB_C128;
+  if (int rc = reserve_phase_buffers(ws, cx, bmax, std::max(64, pivot_nmax(bmax)), count, m)) return rc;
+  const int tile = gram_tile(bmax);
+  const int tiles = (bmax + tile - 1) / tile;
+  GramArgs g{};
+  g.G = G;
+  g.ldg = ldg;
+  g.m = m;
+  g.items = static_cast<const Item *>(ws.items.p);
+  g.count = count;
+  g.bmax = bmax;
+  g.splits = gram_splits(count, tiles, m, gram_kc(cx), &g.ksplit);
+  g.Apart = ws.Apart.p;
+  g.Dpart = static_cast<double *>(ws.Dpart.p);
+  g.A = A;
+  g.D = D;
+  g.tickets = static_cast<unsigned *>(ws.tickets.p);
+  CK(launch_gram(cx, g, st));
+  CK(cudaStreamSynchronize(st));
+  return HJB_OK;
+}
+
+int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_t *items_host, int32_t count,
+              int32_t bmax, const void *A, const double *D, const int8_t *signs_dev, double orth_tol,
+              double quad_tol, int32_t max_sweeps, void *W, int64_t *stats, void *R_out, int32_t cluster,
+              void *stream) {
+  if (count < 1 || bmax < 1 || !A || !D || !W || !stats || !signs_dev || max_sweeps < 1)
+    return fail(HJB_EINVAL, "hjb_pivot: bad arguments");
+  const int nmax = pivot_nmax(bmax);
+  if (nmax < 0) return fail(HJB_EINVAL, "hjb_pivot: block width too large");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  Workspace &ws = g_ws[dev];
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = upload_items(ws, items_host, count, st)) return rc;
+  PivotArgs pa{};
+  pa.G = G;
+  pa.ldg = ldg;
+  pa.m = m;
+  pa.items = static_cast<const Item *>(ws.items.p);
+  pa.count = count;
+  pa.bmax = bmax;
+  pa.A = const_cast<void *>(A);
+  pa.D = D;
+  pa.signs = signs_dev;
+  pa.orth_tol = orth_tol;
+  pa.quad_tol = quad_tol;
+  pa.max_sweeps = max_sweeps;
+  pa.W = W;
+  pa.stats = stats;
+  pa.Rout = R_out;
+  pa.nmax = nmax;
+  cudaError_t e = launch_pivot(dtype == HJB_C128, pa, cluster, st, nullptr);
+  if (e == cudaErrorInvalidConfiguration) return fail(HJB_EINVAL, "hjb_pivot: unsupported cluster size");
+  CK(e);
+  CK(cudaStreamSynchronize(st));
+  return HJB_OK;
+}
+
+int hjb_update(int32_t dtype, int64_t m, void *G, int64_t ldg, const int32_t *items_host, int32_t count,
+               int32_t bmax, const void *W, const int64_t *stats, void *stream) {
+  if (count < 1 || bmax < 1 || !G || !W || !stats) return fail(HJB_EINVAL, "hjb_update: bad arguments");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  Workspace &ws = g_ws[dev];
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = upload_items(ws, items_host, count, st)) return rc;
+  UpdateArgs u{};
+  u.G = G;
+  u.ldg = ldg;
+  u.m = m;
+  u.items = static_cast<const Item *>(ws.items.p);
+  u.count = count;
+  u.nmax = pivot_nmax(bmax);
+  u.W = W;
+  u.stats = stats;
+  CK(launch_update(dtype == HJB_C128, u, st));
+  CK(cudaStreamSynchronize(st));
+  return HJB_OK;
+}
+
+int hjb_extract(int32_t dtype, int64_t m, int64_t n, const void *G, int64_t ldg, const int8_t *signs_dev,
+                double *lam, void *U, int64_t ldu, const int64_t *perm, void *stream) {
+  if (m < 1 || n < 0 || !G || !lam || !U || !signs_dev) return fail(HJB_EINVAL, "hjb_extract: bad arguments");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  Workspace &ws = g_ws[dev];
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(ws.flag.reserve(sizeof(int)));
+  CK(cudaMemsetAsync(ws.flag.p, 0, sizeof(int), st));
+  CK(launch_extract(dtype == HJB_C128, m, n, G, ldg, signs_dev, lam, U, ldu, perm,
+                    static_cast<int *>(ws.flag.p), st));
+  int zf = 0;
+  CK(cudaMemcpyAsync(&zf, ws.flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (zf) return fail(HJB_CHOL_FAIL, "zero-norm column: factor is rank deficient");
+  return HJB_OK;
+}
+
+}  // extern "C"

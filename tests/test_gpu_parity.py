@@ -1,0 +1,303 @@
+"""GPU parity of the B200 path against the CPU oracle and the reference's
+golden vectors.  Every call goes through the C ABI (libhjb200.so)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden, random_full_rank, small_solve_cases
+
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(np.float64).eps
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_1008_4166_b200 as P
+
+    if P._lib.lib().hjb_device_count() < 1:
+        pytest.skip("no CUDA device")
+    return P
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    return t
+
+
+def dev_colmajor(torch, A):
+    A = np.asfortranarray(A)
+    return torch.from_numpy(A.T.copy()).cuda().t()
+
+
+def host(torch, T):
+    return np.asfortranarray(T.t().contiguous().cpu().numpy().T)
+
+
+def items_array(items):
+    return np.ascontiguousarray(np.array(items, np.int32).reshape(-1, 4))
+
+
+# --------------------------------------------------------------------- kernels
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("m,bmax,widths", [(512, 32, [32, 32]), (1000, 64, [64, 64]),
+                                            (77, 16, [16, 15]), (4096, 128, [128, 128]),
+                                            (300, 64, [63, 64])])
+def test_gram_kernel(pkg, torch, cplx, m, bmax, widths):
+    rng = np.random.default_rng(1)
+    n = 4 * bmax
+    G = rng.standard_normal((m, n)) + (1j * rng.standard_normal((m, n)) if cplx else 0)
+    Gd = dev_colmajor(torch, G)
+    ni, nj = widths
+    items = items_array([[0, ni, 2 * bmax, nj], [bmax, ni, 3 * bmax, nj], [bmax, ni, 0, 0]])
+    cnt = items.shape[0]
+    A = torch.zeros(cnt * bmax * bmax, dtype=Gd.dtype, device="cuda")
+    D = torch.zeros(cnt * 2 * bmax, dtype=torch.float64, device="cuda")
+    L = pkg._lib.lib()
+    rc = L.hjb_gram(1 if cplx else 0, m, Gd.data_ptr(), m, items.ctypes.data, cnt, bmax, A.data_ptr(),
+                    D.data_ptr(), None)
+    pkg._lib.check(rc)
+    A = A.cpu().numpy().reshape(cnt, bmax, bmax)
+    D = D.cpu().numpy().reshape(cnt, 2 * bmax)
+    for t, (oi, wi, oj, wj) in enumerate(items):
+        X = G[:, oi:oi + wi]
+        Y = G[:, oj:oj + wj] if wj else X
+        ref = X.conj().T @ Y
+        got = A[t].T[:wi, :ref.shape[1]]  # stored column-major
+        scale = np.linalg.norm(X, axis=0)[:, None] * np.linalg.norm(Y, axis=0)[None, :]
+        assert np.max(np.abs(got - ref) / scale) < 8 * m * EPS
+        if wj:
+            assert np.allclose(D[t, :wi], O.column_norms2(X), rtol=8 * m * EPS)
+            assert np.allclose(D[t, bmax:bmax + wj], O.column_norms2(Y), rtol=8 * m * EPS)
+
+
+def _pivot(pkg, torch, cplx, G, J, items, bmax, cluster=0, max_sweeps=30, orth_tol=None):
+    m = G.shape[0]
+    Gd = dev_colmajor(torch, G)
+    cnt = items.shape[0]
+    L = pkg._lib.lib()
+    A = torch.zeros(cnt * bmax * bmax, dtype=Gd.dtype, device="cuda")
+    D = torch.zeros(cnt * 2 * bmax, dtype=torch.float64, device="cuda")
+    pkg._lib.check(L.hjb_gram(1 if cplx else 0, m, Gd.data_ptr(), m, items.ctypes.data, cnt, bmax,
+                              A.data_ptr(), D.data_ptr(), None))
+    nmax = L.hjb_pivot_ld(bmax)
+    W = torch.zeros(cnt * nmax * nmax, dtype=Gd.dtype, device="cuda")
+    R = torch.zeros(cnt * nmax * nmax, dtype=Gd.dtype, device="cuda")
+    stats = torch.zeros(cnt * 8, dtype=torch.int64, device="cuda")
+    sd = torch.from_numpy(np.ascontiguousarray(J, np.int8)).cuda()
+    rc = L.hjb_pivot(1 if cplx else 0, m, Gd.data_ptr(), m, items.ctypes.data, cnt, bmax, A.data_ptr(),
+                     D.data_ptr(), sd.data_ptr(), orth_tol or -1.0, -1.0, max_sweeps, W.data_ptr(),
+                     stats.data_ptr(), R.data_ptr(), cluster, None)
+    pkg._lib.check(rc)
+    W = W.cpu().numpy().reshape(cnt, nmax, nmax).transpose(0, 2, 1)
+    R = R.cpu().numpy().reshape(cnt, nmax, nmax).transpose(0, 2, 1)
+    return W, R, stats.cpu().numpy().reshape(cnt, 8), Gd
+
+
+def _orthonormal_blocks(rng, m, widths, cplx):
+    """G whose blocks have orthogonal columns (as after the 2F pre-pass)."""
+    cols = []
+    for w in widths:
+        X = rng.standard_normal((m, w)) + (1j * rng.standard_normal((m, w)) if cplx else 0)
+        Q, _ = np.linalg.qr(X)
+        cols.append(Q * rng.uniform(0.5, 3.0, w)[None, :])
+    return np.asfortranarray(np.concatenate(cols, axis=1))
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("b,cluster", [(16, 0), (32, 0), (32, 2), (64, 0), (64, 4), (128, 0)])
+def test_pivot_kernel_matches_oracle(pkg, torch, cplx, b, cluster):
+    """Structured Cholesky + tournament J-Jacobi vs the oracle's same-order
+    restatement (blocking.py:115-138, rotations.py:203-223)."""
+    rng = np.random.default_rng(7 + b)
+    m = 4 * b
+    G = _orthonormal_blocks(rng, m, [b, b], cplx)
+    J = np.array([1] * (b + b // 3) + [-1] * (b - b // 3), np.int8)
+    items = items_array([[0, b, b, b]])
+    W, R, st, _ = _pivot(pkg, torch, cplx, G, J, items, b, cluster=cluster)
+    assert st[0, 4] == 0, st[0]
+    Gi, Gj = G[:, :b], G[:, b:]
+    R0 = O.structured_cholesky(O.column_norms2(Gi), O.gram(Gi, Gj), O.column_norms2(Gj))
+    Rref = R0.copy(order="F")
+    Wref, sw, nrot, nbig, mt, conv = O.diagonalize(Rref, J, order="tournament")
+    N = 2 * b
+    Wg, Rg = W[0, :N, :N], R[0, :N, :N]
+    # same order, same formulas: agreement to rounding
+    assert np.max(np.abs(Wg - Wref)) <= 1e-10 * max(1.0, np.abs(Wref).max())
+    assert np.max(np.abs(Rg - Rref)) <= 1e-10 * np.abs(Rref).max()
+    assert abs(int(st[0, 3]) - sw) <= 1
+    # W is J-unitary and R0 W = R_final (test_rotations.py:201-209)
+    Jf = np.diag(J.astype(float))
+    assert np.abs(Wg.conj().T @ Jf @ Wg - Jf).max() <= 64 * N * EPS * np.linalg.norm(Wg, 2) ** 2
+    assert np.abs(R0 @ Wg - Rg).max() <= 1e-11 * np.abs(R0).max() * np.linalg.norm(Wg, 2)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_pivot_dense_prepass_mode(pkg, torch, cplx):
+    rng = np.random.default_rng(3)
+    b, m = 32, 200
+    G = random_full_rank(rng, m, b, cplx)
+    J = np.array([1] * 20 + [-1] * 12, np.int8)
+    W, R, st, _ = _pivot(pkg, torch, cplx, G, J, items_array([[0, b, 0, 0]]), b)
+    R0 = O.chol_upper(O.gram(G))
+    Rref = R0.copy(order="F")
+    Wref, *_ = O.diagonalize(Rref, J, order="tournament")
+    assert np.max(np.abs(W[0, :b, :b] - Wref)) <= 1e-10 * max(1.0, np.abs(Wref).max())
+
+
+def test_update_kernel(pkg, torch):
+    rng = np.random.default_rng(11)
+    for cplx in (False, True):
+        for b in (16, 32, 64, 128):
+            m = 333
+            G = random_full_rank(rng, m, 4 * b, cplx)
+            Gd = dev_colmajor(torch, G)
+            items = items_array([[0, b, 3 * b, b], [2 * b, b, b, b]])
+            L = pkg._lib.lib()
+            nmax = L.hjb_pivot_ld(b)
+            Wh = rng.standard_normal((2, 2 * b, 2 * b)) + (1j * rng.standard_normal((2, 2 * b, 2 * b)) if cplx else 0)
+            Wpad = np.zeros((2, nmax, nmax), dtype=Wh.dtype)
+            Wpad[:, :2 * b, :2 * b] = Wh
+            Wd = torch.from_numpy(np.ascontiguousarray(Wpad.transpose(0, 2, 1))).cuda()
+            stats = torch.ones(2 * 8, dtype=torch.int64, device="cuda")
+            pkg._lib.check(L.hjb_update(1 if cplx else 0, m, Gd.data_ptr(), m, items.ctypes.data, 2, b,
+                                        Wd.data_ptr(), stats.data_ptr(), None))
+            out = host(torch, Gd)
+            ref = G.copy()
+            for t, (oi, wi, oj, wj) in enumerate(items):
+                X = np.concatenate([G[:, oi:oi + wi], G[:, oj:oj + wj]], axis=1)
+                Y = X @ Wh[t]
+                ref[:, oi:oi + wi] = Y[:, :wi]
+                ref[:, oj:oj + wj] = Y[:, wi:]
+            assert np.max(np.abs(out - ref)) <= 1e-12 * np.abs(ref).max() * 4 * b
+
+
+# --------------------------------------------------------------------- whole path
+
+@pytest.mark.parametrize("case", small_solve_cases(), ids=lambda c: f"c{c['k']}")
+def test_small_solves_vs_reference_golden(pkg, case):
+    cfg = pkg.SolverConfig(variant="2F", strategy=case["strategy"], p=case["p"],
+                           tol=pkg.Tolerances(orth_tol=case["orth_tol"], max_sweeps=case["max_sweeps"]))
+    Gout, info = pkg.parallel_jacobi(case["G"], case["J"], cfg)
+    assert info.converged == case["converged"]
+    if not case["converged"]:
+        assert info.sweeps == case["sweeps"]
+        return
+    assert abs(info.sweeps - case["sweeps"]) <= 1
+    n = case["G"].shape[1]
+    lam = np.sort(case["J"] * O.column_norms2(Gout))
+    ref = np.sort(case["J"] * O.column_norms2(case["Gout"]))
+    kappa = math.sqrt(O.scaled_condition(O.gram(case["G"])))
+    assert np.all(np.abs(lam - ref) <= 64 * n * EPS * kappa * np.abs(ref))
+    if case["rotations"] == 0:
+        assert np.array_equal(Gout, case["G"])  # column order restored bit-exactly
+
+
+def _residual_check(G0, J, Gout, n):
+    H = G0 @ np.diag(J.astype(float)) @ G0.conj().T
+    lam, U = O.extract_eigen(Gout, J)
+    hn = np.abs(lam).max()
+    res = np.linalg.norm(H @ U - U * lam, axis=0) / (hn * np.linalg.norm(U, axis=0))
+    return res.max()
+
+
+def test_cfg1_full_size(pkg):
+    from paper_1008_4166_b200 import workloads
+
+    z = golden("config_proxies.npz")
+    w = workloads.cfg1()
+    cfg = pkg.SolverConfig(variant="2F", strategy="round_robin", p=w.p,
+                           tol=pkg.Tolerances(orth_tol=w.orth_tol))
+    Gout, info = pkg.parallel_jacobi(w.G, w.J, cfg)
+    ref = np.sort(z["cfg1_n512_b32_lam"])
+    lam = np.sort(w.J * O.column_norms2(Gout))
+    kappa = math.sqrt(O.scaled_condition(O.gram(w.G)))
+    assert np.all(np.abs(lam - ref) <= 64 * w.n * EPS * kappa * np.abs(ref))
+    assert info.converged and abs(info.sweeps - int(z["cfg1_n512_b32_info"][0])) <= 1
+    assert _residual_check(w.G, w.J, Gout, w.n) <= 64 * w.n * EPS
+
+
+@pytest.mark.parametrize("name,kw", [("cfg2", {"n": 512, "b": 32}), ("cfg3", {"n": 512, "b": 32}),
+                                     ("cfg5r", {"n": 512, "b": 64})])
+def test_config_proxies(pkg, name, kw):
+    from paper_1008_4166_b200 import workloads
+
+    z = golden("config_proxies.npz")
+    w = workloads.make(name, **kw)
+    key = f"{name}_n{w.n}_b{w.b}"
+    cfg = pkg.SolverConfig(variant="2F", strategy="round_robin", p=w.p,
+                           tol=pkg.Tolerances(orth_tol=w.orth_tol))
+    Gout, info = pkg.parallel_jacobi(w.G, w.J, cfg)
+    ref = np.sort(z[key + "_lam"])
+    lam = np.sort(w.J * O.column_norms2(Gout))
+    kappa = math.sqrt(O.scaled_condition(O.gram(w.G)))
+    assert np.all(np.abs(lam - ref) <= 64 * w.n * EPS * kappa * np.abs(ref))
+    assert info.converged and abs(info.sweeps - int(z[key + "_info"][0])) <= 1
+    assert _residual_check(w.G, w.J, Gout, w.n) <= 64 * w.n * EPS
+
+
+def test_determinism_bitwise(pkg, rng):
+    G = random_full_rank(rng, 96, 96, True)
+    J = np.array([1] * 60 + [-1] * 36, np.int8)
+    cfg = pkg.SolverConfig(variant="2F", strategy="modulus", p=3)
+    a, ia = pkg.parallel_jacobi(G, J, cfg)
+    b, ib = pkg.parallel_jacobi(G, J, cfg)
+    assert np.array_equal(a, b) and ia.rotations == ib.rotations
+
+
+def test_device_tensor_io(pkg, torch, rng):
+    G = random_full_rank(rng, 64, 64, False)
+    J = np.array([1] * 40 + [-1] * 24, np.int8)
+    cfg = pkg.SolverConfig(variant="2F", strategy="round_robin", p=4)
+    a, _ = pkg.parallel_jacobi(G, J, cfg)
+    Gd = dev_colmajor(torch, G)
+    b, _ = pkg.parallel_jacobi(Gd, J, cfg)
+    assert b.is_cuda and np.array_equal(host(torch, b), a)
+    assert np.array_equal(host(torch, Gd), G)  # input untouched
+
+
+def test_extract_eigen_gpu(pkg, rng):
+    G = random_full_rank(rng, 40, 40, True)
+    J = np.array([1] * 25 + [-1] * 15, np.int8)
+    for perm, desc in ((None, False), (None, True), (rng.permutation(40), False), (rng.permutation(40), True)):
+        r = pkg.extract_eigen(G, J, col_perm=perm, sort_descending=desc)
+        lam, U = O.extract_eigen(G, J, col_perm=perm, sort_descending=desc)
+        assert np.allclose(r.eigenvalues, lam, rtol=1e-14, atol=0)
+        assert np.allclose(r.eigenvectors, U, rtol=1e-13, atol=1e-15)
+    Z = G.copy()
+    Z[:, 3] = 0
+    with pytest.raises(pkg.StructuralError):
+        pkg.extract_eigen(Z, J)
+
+
+def test_zero_column_raises_definiteness(pkg, rng):
+    G = random_full_rank(rng, 16, 16, False)
+    G[:, 3] = 0.0
+    with pytest.raises(pkg.DefinitenessError):
+        pkg.parallel_jacobi(G, np.ones(16, np.int8), pkg.SolverConfig(variant="2F", p=2))
+
+
+def test_duplicate_column_raises_structural(pkg, rng):
+    G = random_full_rank(rng, 16, 16, False)
+    G[:, 5] = G[:, 2]
+    with pytest.raises(pkg.StructuralError):
+        pkg.parallel_jacobi(G, np.ones(16, np.int8), pkg.SolverConfig(variant="2F", p=2))
+
+
+def test_cluster_sizes_agree(pkg, torch):
+    """Different cluster splittings of one pivot agree to rounding."""
+    rng = np.random.default_rng(5)
+    b = 64
+    J = np.array([1] * 70 + [-1] * 58, np.int8)
+    items = items_array([[0, b, b, b]])
+    for cplx, clusters in ((False, (2, 4, 8)), (True, (4, 8))):
+        G = _orthonormal_blocks(rng, 256, [b, b], cplx)
+        outs = [_pivot(pkg, torch, cplx, G, J, items, b, cluster=c)[0][0] for c in clusters]
+        for W in outs[1:]:
+            assert np.max(np.abs(W - outs[0])) <= 1e-10 * np.abs(outs[0]).max()

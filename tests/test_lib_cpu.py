@@ -1,0 +1,90 @@
+"""CPU-side checks of the native library: it loads, exports every symbol the
+C header declares, its ring schedule is bit-exact with the reference's, and
+argument validation matches the reference's ValueErrors.  No GPU needed."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+import paper_1008_4166_b200 as P
+from paper_1008_4166_b200 import _lib, strategies
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "hjb200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(hjb_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for name in syms:
+        assert hasattr(L, name), name
+        assert name in _lib.SIGNATURES, name
+    assert L.hjb_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("strategy", ["modulus", "round_robin"])
+@pytest.mark.parametrize("p", list(range(1, 9)) + [16, 32, 64])
+def test_native_schedule_bit_exact(strategy, p):
+    z = golden("schedules.npz")
+    lay_ref = z[f"{strategy}_p{p}_layouts"]
+    plans_ref = z[f"{strategy}_p{p}_plans"]
+    sweeps = lay_ref.shape[0] // strategies.steps_per_sweep(strategy, p)
+    lay, plans = strategies.schedule_arrays(strategy, p, sweeps)
+    assert np.array_equal(lay, lay_ref)
+    assert np.array_equal(plans, plans_ref)
+
+
+def test_schedule_period_two_sweeps():
+    """Layouts repeat every 2 sweeps for the config sizes."""
+    for strategy in ("modulus", "round_robin"):
+        for p in (8, 16, 32, 64, 128):
+            lay, _ = strategies.schedule_arrays(strategy, p, 4)
+            s = strategies.steps_per_sweep(strategy, p)
+            assert np.array_equal(lay[:2 * s], lay[2 * s:])
+
+
+def test_steps_per_sweep_native():
+    L = _lib.lib()
+    assert L.hjb_steps_per_sweep(0, 3) == 6 and L.hjb_steps_per_sweep(1, 3) == 5
+    assert L.hjb_steps_per_sweep(1, 0) == -1
+
+
+def test_validation_errors_match_reference():
+    rng = np.random.default_rng(0)
+    G = rng.standard_normal((4, 4))
+    J = np.ones(4, np.int8)
+    with pytest.raises(ValueError):
+        P.SolverConfig(variant="4X")
+    with pytest.raises(ValueError):
+        P.SolverConfig(variant="2F", p=0)
+    assert P.SolverConfig(variant="2F", strategy="rr").strategy == "round_robin"
+    with pytest.raises(ValueError):  # parallel.py:264-265
+        P.parallel_jacobi(G, J, P.SolverConfig(variant="2F", p=3))
+    with pytest.raises(ValueError):
+        P.parallel_jacobi(G, np.array([1, 2, 1, 1]), P.SolverConfig(variant="2F", p=1))
+    with pytest.raises(ValueError):  # B variants are not on the B200 path
+        P.parallel_jacobi(G, J, P.SolverConfig(variant="2B", p=1))
+
+
+def test_uniform_partition_matches_reference_rule():
+    part = P.uniform_partition(20, 6)
+    assert part.sizes == (4, 4, 3, 3, 3, 3) and part.offsets[-1] == 20
+    with pytest.raises(ValueError):
+        P.uniform_partition(3, 4)
+
+
+def test_generate_sweep_schedule_surface():
+    lay = P.generate_sweep_schedule("rr", 3, 1)
+    assert len(lay) == 5 and lay[0] == [(1, 6), (2, 5), (3, 4)]
