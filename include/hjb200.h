@@ -150,6 +150,12 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
 
 /* Leading dimension of W / R_out used by hjb_pivot for a given bmax. */
 int hjb_pivot_ld(int32_t bmax);
+/* Debug: record per-CTA phase clocks of later hjb_pivot calls into a device
+ * int64 buffer [count*cluster][8] (NULL disables). */
+int hjb_pivot_set_profile(void *prof);
+/* Tuning override for the pivot kernel: threads per CTA (256/512/1024) and
+ * cluster size (1..16); 0 restores the automatic choice. */
+int hjb_tune(int32_t pivot_threads, int32_t pivot_cluster);
 
 /*
  * Block update [G_i G_j] <- [G_i G_j] W for items whose stats[0] > 0

@@ -70,6 +70,8 @@ SIGNATURES = {
                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "hjb_pivot_ld": (C.c_int, [C.c_int32]),
+    "hjb_pivot_set_profile": (C.c_int, [C.c_void_p]),
+    "hjb_tune": (C.c_int, [C.c_int32, C.c_int32]),
     "hjb_update": (C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hjb_comm_unique_id": (C.c_int, [C.c_void_p]),

@@ -60,6 +60,18 @@ __device__ __forceinline__ double shfl_xor(double v, int m) { return __shfl_xor_
 __device__ __forceinline__ cplx shfl_xor(cplx v, int m) {
   return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
 }
+__device__ __forceinline__ double shfl_down(double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ cplx shfl_down(cplx v, int d) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
+__device__ __forceinline__ double shfl_up(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ cplx shfl_up(cplx v, int d) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+__device__ __forceinline__ double shfl_idx(double v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+__device__ __forceinline__ cplx shfl_idx(cplx v, int l) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, l), __shfl_sync(0xffffffffu, v.y, l));
+}
 __device__ __forceinline__ bool finite_pos(double d) { return d > 0.0 && d <= 1.79769313486231570e308; }
 
 // ---- FP64 tensor-core tile: D(8x8) += A(8x4, row) * B(4x8, col) ----

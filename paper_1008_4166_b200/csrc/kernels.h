@@ -41,11 +41,14 @@ struct PivotArgs {
   int64_t *stats;     // [count][ST_N]
   void *Rout;         // optional [count][nmax*nmax]
   int nmax;
+  long long *prof;    // optional per-CTA phase clocks [count*C][8] (debug)
 };
 // cluster: 0 = automatic choice
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used);
 int pivot_nmax(int bmax);   // NMAX instance for a block width
-int pivot_default_cluster(bool cx, int nmax);
+int pivot_default_cluster(bool cx, int nmax, int count);
+int pivot_default_threads(bool cx, int nmax, int cluster);
+void pivot_tune(int threads, int cluster);  // 0 = automatic
 
 struct UpdateArgs {
   void *G;

@@ -27,6 +27,7 @@
 // its own rows.  One cluster barrier per round.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 
@@ -51,12 +52,17 @@ struct PivCfg {
   static_assert(TPP >= 1 && TPP <= 32 && (TPP & (TPP - 1)) == 0, "threads per pair");
   static_assert(RPT >= 1 && RPC % TPP == 0, "rows per thread");
   static_assert(OPT >= 1 && (RPC * NMAX) % NT == 0, "outputs per thread");
-  static_assert(HC * NMAX <= NMAX * RS, "scratch fits in the W slab");
+  static constexpr int NWARP = NT / 32;
+  static constexpr int SPW = 32 / TPP;                       // pair slots per warp
+  static constexpr int XBUF = 2 * NWARP * RPC;               // [parity][warp][row]
+  static constexpr int SCR0 = HC * NMAX > XBUF ? HC * NMAX : XBUF;
+  static constexpr int SCR = SCR0 > NMAX * RS ? SCR0 : NMAX * RS;   // also the R_final / W slab
   // shared-memory carve-up (bytes, 16-aligned)
   static constexpr size_t OFF_R = 0;
-  static constexpr size_t OFF_W = OFF_R + size_t(NMAX) * RS * sizeof(T);
-  static constexpr size_t OFF_PART = OFF_W + size_t(NMAX) * RS * sizeof(T);
-  static constexpr size_t OFF_ROW = OFF_PART + 2 * size_t(P2) * sizeof(T);
+  static constexpr size_t OFF_W = OFF_R + size_t(NMAX) * RS * sizeof(T);  // scratch
+  static constexpr size_t OFF_PART = OFF_W + size_t(SCR) * sizeof(T);
+  static constexpr size_t PART = (2 * C * P2 > RPC * NMAX) ? 2 * C * P2 : RPC * NMAX;  // also W-block scratch
+  static constexpr size_t OFF_ROW = OFF_PART + PART * sizeof(T);
   static constexpr size_t OFF_NPART = OFF_ROW + 2 * size_t(NMAX) * sizeof(T);
   static constexpr size_t OFF_D = OFF_NPART + NMAX * sizeof(double);
   static constexpr size_t OFF_LAM = OFF_D + NMAX * sizeof(double);
@@ -64,12 +70,16 @@ struct PivCfg {
   static constexpr size_t SMEM = OFF_J + NMAX * sizeof(int);
 };
 
+// cluster-scope barrier with release/acquire semantics only (cg's sync()
+// adds a gpu-scope MEMBAR that the DSMEM exchanges here do not need)
 template <int C>
 __device__ __forceinline__ void cluster_sync() {
-  if constexpr (C > 1)
-    cg::this_cluster().sync();
-  else
+  if constexpr (C > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
     __syncthreads();
+  }
 }
 
 template <int C, typename P>
@@ -80,67 +90,112 @@ __device__ __forceinline__ P *remote(P *p, int rank) {
     return p;
 }
 
+// ---- cluster partial-dot exchange: st.async into peer smem + mbarrier ----
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t *bar, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "HJB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HJB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t raddr, cplx v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "l"(__double_as_longlong(v.x)), "l"(__double_as_longlong(v.y)), "r"(rbar)
+               : "memory");
+}
+
+// Rotation coefficients with the phase folded in: [x_r, x_s] <-
+// [cp x_r + hs x_s, sp x_r + cs x_s], cp = cs*phase, sp = sn*phase,
+// hs = hyp*sn -- algebraically _kernels.py:82-92.
 template <typename T>
-struct RotParams {
+struct RotCoef {
   int code;  // 0 skip, 1 rotate, -1 indefinite pivot
-  double cs, sn, t, eta, hyp;
-  T phase;
+  double cs, hs, num, den, eta, hyp;  // t = num / den (kept off the dependency chain)
+  T cp, sp;
 };
 
-__device__ __forceinline__ double absv(double a) { return fabs(a); }
-__device__ __forceinline__ double absv(cplx a) { return hypot(a.x, a.y); }
+__device__ __forceinline__ double phase_mul(double a, double s) { return a * s; }
+__device__ __forceinline__ cplx phase_mul(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
 
-// _kernels.py:53-81 for one pair (a = g_r^H g_s, dr/ds = cached Gram diagonal)
+// _kernels.py:53-81 restated for a short dependency chain.  With q = |a|^2,
+// e = 2*eta (e^2 = 4q) and delta = d_s - d_r:
+//   trig:       t = sgn(theta)|e| / (|delta| + sqrt(delta^2 + 4q))
+//   hyperbolic: t = -e / (s + sqrt(s^2 - 4q)),  s = d_r + d_s
+// and cs = den / sqrt(den^2 +- 4q), sn = num / sqrt(den^2 +- 4q).  The chain
+// is q -> sqrt -> rsqrt (|a| and the phase come from an independent rsqrt);
+// s^2 - 4q and den^2 - 4q are single-rounding FMAs.
 template <typename T>
-__device__ __forceinline__ RotParams<T> rot_params(T a, double dr, double ds, bool same, double otol) {
-  RotParams<T> p;
-  p.code = 0;
-  p.cs = 1.0; p.sn = 0.0; p.t = 0.0; p.eta = 0.0; p.hyp = 0.0;
-  p.phase = S<T>::one();
-  const double aa = absv(a);
-  if (aa <= otol * sqrt(dr * ds)) return p;
-  if (aa * aa >= dr * ds) { p.code = -1; return p; }
-  const double eta = re(a) >= 0.0 ? aa : -aa;
-  p.phase = divr(a, eta);
-  double t, h;
-  if (same) {
-    p.hyp = -1.0;
-    const double theta = (ds - dr) / (2.0 * eta);
-    const double sg = theta >= 0.0 ? 1.0 : -1.0;
-    t = sg / (fabs(theta) + sqrt(theta * theta + 1.0));
-    h = sqrt(1.0 + t * t);
-  } else {
-    p.hyp = 1.0;
-    const double theta = -(dr + ds) / (2.0 * eta);
-    const double disc = theta * theta - 1.0;
-    if (disc <= 0.0) { p.code = -1; return p; }
-    const double sg = theta >= 0.0 ? 1.0 : -1.0;
-    t = sg / (fabs(theta) + sqrt(disc));
-    h = sqrt(1.0 - t * t);
-  }
-  p.cs = 1.0 / h;
-  p.sn = p.cs * t;
-  p.t = t;
-  p.eta = eta;
-  p.code = 1;
+__device__ __forceinline__ RotCoef<T> rot_coef(T a, double dr, double ds, bool same, double otol2) {
+  // branch-free: both rotation kinds share den = |x| + sqrt(x^2 +- 4q),
+  // r = rsqrt(den^2 +- 4q) with x = d_s - d_r (trig, +) or d_r + d_s (hyp, -)
+  RotCoef<T> p;
+  const double q = abs2(a);
+  const double dd = dr * ds;
+  const double q4 = 4.0 * q;
+  const double ri = rsqrt(q);
+  const double sa = re(a) >= 0.0 ? 1.0 : -1.0;
+  const double aa = q * ri;
+  const double x = same ? ds - dr : dr + ds;
+  const double sq4 = same ? q4 : -q4;
+  const double disc = fma(x, x, sq4);
+  const double den = fabs(x) + sqrt(fmax(disc, 0.0));
+  const double r = rsqrt(fma(den, den, sq4));
+  const bool pos = x == 0.0 || ((x > 0.0) == (sa > 0.0));
+  const double num = same ? (pos ? 2.0 * aa : -2.0 * aa) : -2.0 * sa * aa;
+  const bool skip = q <= otol2 * dd;                     // _kernels.py:57
+  const bool bad = q >= dd || (!same && disc <= 0.0);   // _kernels.py:59-60, 73-74
+  p.code = skip ? 0 : (bad ? -1 : 1);
+  p.hyp = same ? -1.0 : 1.0;
+  const double cs = den * r, sn = num * r;
+  const T ph = phase_mul(a, sa * ri);
+  p.cs = cs;
+  p.hs = p.hyp * sn;
+  p.cp = phase_mul(ph, cs);
+  p.sp = phase_mul(ph, sn);
+  p.num = num;
+  p.den = den;
+  p.eta = sa * aa;
   return p;
 }
 
-// [x_r, x_s] <- [cs*(phase x_r) + hyp*sn*x_s, sn*(phase x_r) + cs*x_s]  (_kernels.py:82-92)
 template <typename T>
-__device__ __forceinline__ void rot_apply(T &xr, T &xs, const RotParams<T> &p) {
-  const T f = mul(p.phase, xr);
-  const double hs = p.hyp * p.sn;
-  const T nr = add(scale(f, p.cs), scale(xs, hs));
-  const T ns = add(scale(f, p.sn), scale(xs, p.cs));
+__device__ __forceinline__ void rot_fold(T &xr, T &xs, const RotCoef<T> &p);
+template <>
+__device__ __forceinline__ void rot_fold<double>(double &xr, double &xs, const RotCoef<double> &p) {
+  const double nr = fma(p.cp, xr, p.hs * xs);
+  const double ns = fma(p.sp, xr, p.cs * xs);
   xr = nr;
   xs = ns;
 }
 template <>
-__device__ __forceinline__ void rot_apply<double>(double &xr, double &xs, const RotParams<double> &p) {
-  const double f = p.phase * xr;
-  const double nr = p.cs * f + (p.hyp * p.sn) * xs;
-  const double ns = p.sn * f + p.cs * xs;
+__device__ __forceinline__ void rot_fold<cplx>(cplx &xr, cplx &xs, const RotCoef<cplx> &p) {
+  cplx nr, ns;
+  nr.x = fma(p.cp.x, xr.x, fma(-p.cp.y, xr.y, p.hs * xs.x));
+  nr.y = fma(p.cp.x, xr.y, fma(p.cp.y, xr.x, p.hs * xs.y));
+  ns.x = fma(p.sp.x, xr.x, fma(-p.sp.y, xr.y, p.cs * xs.x));
+  ns.y = fma(p.sp.x, xr.y, fma(p.sp.y, xr.x, p.cs * xs.y));
   xr = nr;
   xs = ns;
 }
@@ -164,9 +219,15 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   __shared__ int s_big;
   __shared__ int s_fail;
   __shared__ unsigned long long s_maxt;
+  __shared__ uint64_t s_mbar[2];
+  __shared__ int cib[NMAX / 2], cjb[NMAX / 2], k_on[NMAX / 2];
+  __shared__ double k_cs[NMAX / 2], k_hs[NMAX / 2];
+  __shared__ T k_cp[NMAX / 2], k_sp[NMAX / 2];
 
   int crank = 0;
   if constexpr (C > 1) crank = int(cg::this_cluster().block_rank());
+  const long long t_start = clock64();
+  long long t_chol = 0, t_jac = 0;
   const int item_id = blockIdx.x / C;
   const Item it = a.items[item_id];
   const int tid = threadIdx.x;
@@ -184,10 +245,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     Jv[c] = c < ni ? a.signs[it.oi + c] : (c < N ? a.signs[it.oj + (c - ni)] : 1);
     lam[c] = (!dense && c < N) ? a.D[int64_t(item_id) * 2 * bmax + (c < ni ? c : bmax + (c - ni))] : 1.0;
   }
-  for (int e = tid; e < NMAX * RS; e += NT) {
-    Rs[e] = S<T>::zero();
-    Ws[e] = S<T>::zero();
-  }
+  for (int e = tid; e < NMAX * RS; e += NT) Rs[e] = S<T>::zero();
   if (tid == 0) { s_fail = INT_MAX; s_maxt = 0ull; s_big = 0; s_cnt[0] = s_cnt[1] = 0; }
   __syncthreads();
 
@@ -230,7 +288,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         const int hc = min(HC, ni - h0);
         for (int e = tid; e < HC * nj; e += NT) {
           const int h = e % HC, l = e / HC;
-          scr[h * NMAX + l] = h < hc ? A[(h0 + h) + int64_t(l) * bmax] : S<T>::zero();
+          scr[h * NMAX + l] = h < hc ? __ldcg(A + (h0 + h) + int64_t(l) * bmax) : S<T>::zero();
         }
         __syncthreads();
 #pragma unroll
@@ -339,106 +397,249 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     if (!cholesky(0)) status = PV_CHOL;
   }
 
+  t_chol = clock64();
   // ------------------------------------------------------------------ Jacobi
-  for (int e = tid; e < NMAX * RS; e += NT) Ws[e] = S<T>::zero();
-  __syncthreads();
-  for (int gl = tid; gl < RPC; gl += NT) {
-    const int g = row0 + gl;
-    if (g < N) Ws[gl + g * RS] = S<T>::one();
-  }
+  // Register-resident columns.  Pair slot q (TPP lanes) holds the RPC-row
+  // slab of two columns of R in registers; lane l owns rows l, l+TPP, ...
+  // After each round the slot keeps one column and passes the other to its
+  // ring neighbour, exactly as the reference's modulus stepper passes block
+  // columns between workers (strategies.py:58-92, applied with nbl = N): a
+  // warp shuffle inside a warp, shared memory across warps.  W is not
+  // accumulated rotation by rotation: the initial factor R0 stays in shared
+  // memory and W = R0^-1 R_final is formed once at the end.
   const double otol = a.orth_tol > 0.0 ? a.orth_tol : sqrt(double(N)) * kEps;
+  const double otol2 = otol * otol;
   const double qtol = a.quad_tol > 0.0 ? a.quad_tol : double(N) * kEps;
   const int ne = N + (N & 1);
-  const int rounds = ne - 1;
+  const int pr = ne / 2;  // ring slots in use
   const int slot = tid / TPP, lane_in = tid % TPP;
+  constexpr int SPW = Cfg::SPW;
+  const bool in_ring = slot < pr;
+  const int wslot = slot % SPW, warp = slot / SPW;
+  int ip = slot + 1, jp = ne - slot, ib = ip, jb = jp;  // strategies.py:58-66
   long long nrot_total = 0;
   int sweeps = 0;
-  int gr = 0;  // global round counter (partial-buffer parity)
-  __syncthreads();
+  int gr = 0;  // global round counter (buffer parities)
+  int my_big = 0, my_cnt = 0;
+  double my_maxt = 0.0;
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int pd_on = 0, pd_ci = 0, pd_cj = 0;
+  double pd_dr = 0, pd_ds = 0, pd_num = 0, pd_den = 1, pd_eta = 0, pd_hyp = 0;
+  auto finish_d = [&]() {
+    const double t = pd_num / pd_den;
+    Dv[pd_ci] = pd_dr + pd_hyp * t * pd_eta;
+    Dv[pd_cj] = pd_ds + t * pd_eta;
+    ++my_cnt;
+    const double at = fabs(t);
+    my_big += at > qtol;
+    my_maxt = fmax(my_maxt, at);
+    pd_on = 0;
+  };
+  T *xbuf = Ws;
+  constexpr unsigned TX = (C - 1) * Cfg::P2 * sizeof(T);  // bytes pushed into each CTA per round
+  if constexpr (C > 1) {
+    if (tid == 0) {
+      for (int b = 0; b < 2; ++b) mbar_init(&s_mbar[b], 1);
+      fence_mbar_init();
+      for (int b = 0; b < 2; ++b) mbar_arm(&s_mbar[b], TX);
+    }
+  }
+  if (in_ring && lane_in == 0) {
+    cib[slot] = ib - 1;
+    cjb[slot] = jb - 1;
+  }
+  T X[RPT], Y[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int row = lane_in + u * TPP;
+    const int ci = in_ring ? ib - 1 : 0, cj = in_ring ? jb - 1 : 1;
+    X[u] = Rs[ci * RS + row];
+    Y[u] = Rs[cj * RS + row];
+  }
+  cluster_sync<C>();
 
   if (status == PV_OK) {
     for (int sw = 0; sw < a.max_sweeps; ++sw) {
       ++sweeps;
-      // D = colnorms^2(R) (rotations.py:217), reduced over the cluster
-      for (int c = tid; c < NMAX; c += NT) {
-        double s = 0.0;
-        for (int gl = 0; gl < RPC; ++gl) s += abs2(Rs[gl + c * RS]);
-        npart[c] = s;
-      }
-      cluster_sync<C>();
-      for (int c = tid; c < NMAX; c += NT) {
-        double s = 0.0;
+      const bool odd = (sw & 1) == 0;  // reference sweeps count from 1; odd send to q-1
+      // D = colnorms^2(R) (rotations.py:217), from the registers, reduced over the cluster
+      {
+        double nx0 = 0.0, nx1 = 0.0, ny0 = 0.0, ny1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          if (u & 1) { nx1 += abs2(X[u]); ny1 += abs2(Y[u]); }
+          else { nx0 += abs2(X[u]); ny0 += abs2(Y[u]); }
+        }
+        double nx = nx0 + nx1, ny = ny0 + ny1;
+#pragma unroll
+        for (int o = 1; o < TPP; o <<= 1) {
+          nx += __shfl_xor_sync(0xffffffffu, nx, o);
+          ny += __shfl_xor_sync(0xffffffffu, ny, o);
+        }
+        if (in_ring && lane_in == 0) {
+          npart[ib - 1] = nx;
+          npart[jb - 1] = ny;
+        }
+        cluster_sync<C>();
+        if (in_ring && lane_in < 2) {
+          const int col = lane_in == 0 ? ib - 1 : jb - 1;
+          double sacc = 0.0;
 #pragma unroll 1
-        for (int q = 0; q < C; ++q) s += remote<C>(npart, q)[c];
-        Dv[c] = s;
+          for (int q = 0; q < C; ++q) sacc += remote<C>(npart, q)[col];
+          Dv[col] = sacc;
+        }
       }
       if (tid == 0) s_cnt[(sw + 1) & 1] = 0;
       __syncthreads();
 
-      for (int rnd = 0; rnd < rounds; ++rnd, ++gr) {
-        int pa, pb;
-        if (slot == 0) {
-          pa = ne - 1;
-          pb = rnd;
-        } else {
-          pa = (rnd + slot) % (ne - 1);
-          pb = (rnd - slot + ne - 1) % (ne - 1);
-        }
-        const int r = min(pa, pb), s = max(pa, pb);
-        const bool active = (slot < ne / 2) && (s < N);
-        const int rr = active ? r : 0, ss = active ? s : 1;
-        T xr[RPT], xs[RPT];
-        T dot = S<T>::zero();
+      for (int rnd = 0; rnd < ne; ++rnd, ++gr) {
+        const long long c0 = clock64();
+        if (pd_on) finish_d();
+        // (1) slab phase: CTA-partial of g_i^H g_j for this slot's pair
+        T d0 = S<T>::zero(), d1 = S<T>::zero();
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
-          const int row = lane_in + u * TPP;
-          xr[u] = Rs[rr * RS + row];
-          xs[u] = Rs[ss * RS + row];
-          dot = cfma(xr[u], xs[u], dot);
+          if (u & 1)
+            d1 = cfma(X[u], Y[u], d1);
+          else
+            d0 = cfma(X[u], Y[u], d0);
         }
+        T dot = add(d0, d1);
 #pragma unroll
         for (int o = 1; o < TPP; o <<= 1) dot = add(dot, shfl_xor(dot, o));
-        if constexpr (C > 1) {
-          const int buf = gr & 1;
-          if (lane_in == 0) part[buf * Cfg::P2 + slot] = dot;
-          cluster_sync<C>();
-          T acc = S<T>::zero();
+        const int buf = gr & 1;
+        {
+          T *mine = part + (buf * C + crank) * Cfg::P2 + slot;
+          if constexpr (C > 1) {
+            const uint32_t la = smem_u32(mine), lb = smem_u32(&s_mbar[buf]);
 #pragma unroll 1
-          for (int q = lane_in; q < C; q += TPP) acc = add(acc, remote<C>(part, q)[buf * Cfg::P2 + slot]);
-#pragma unroll
-          for (int o = 1; o < TPP; o <<= 1) acc = add(acc, shfl_xor(acc, o));
-          dot = acc;
-        }
-        if (active) {
-          const double dr = Dv[rr], ds = Dv[ss];
-          const RotParams<T> p = rot_params<T>(dot, dr, ds, Jv[rr] == Jv[ss], otol);
-          if (p.code == 1) {
-#pragma unroll
-            for (int u = 0; u < RPT; ++u) {
-              const int row = lane_in + u * TPP;
-              rot_apply<T>(xr[u], xs[u], p);
-              Rs[rr * RS + row] = xr[u];
-              Rs[ss * RS + row] = xs[u];
-              T wr = Ws[rr * RS + row], ws = Ws[ss * RS + row];
-              rot_apply<T>(wr, ws, p);
-              Ws[rr * RS + row] = wr;
-              Ws[ss * RS + row] = ws;
+            for (int q = lane_in; q < C; q += TPP) {
+              if (q == crank)
+                *mine = dot;
+              else
+                st_async(mapa_u32(la, q), dot, mapa_u32(lb, q));
             }
-            if (lane_in == 0) {
-              Dv[rr] = dr + p.hyp * p.t * p.eta;
-              Dv[ss] = ds + p.t * p.eta;
-              atomicAdd(&s_cnt[sw & 1], 1);
-              const double at = fabs(p.t);
-              if (at > qtol) atomicAdd(&s_big, 1);
-              atomicMax(&s_maxt, static_cast<unsigned long long>(__double_as_longlong(at)));
-            }
-          } else if (p.code < 0 && lane_in == 0) {
-            atomicMin(&s_fail, r * 4096 + s);
+          } else {
+            if (lane_in == 0) *mine = dot;
           }
         }
+        const long long c1 = clock64();
+        long long c2 = c1, c3 = c1, c4 = c1;
         __syncthreads();
+        // (2) pair phase: one thread per pair sums the cluster partials in
+        // fixed rank order (bit-identical in every CTA), derives the rotation
+        // once and publishes its coefficients
+        if (tid < pr) {
+          const int q = tid;
+          const int ci = cib[q], cj = cjb[q];
+          if constexpr (C > 1) mbar_wait(&s_mbar[buf], (gr >> 1) & 1);
+          c2 = clock64();
+          T acc = part[(buf * C) * Cfg::P2 + q];
+#pragma unroll 1
+          for (int r = 1; r < C; ++r) acc = add(acc, part[(buf * C + r) * Cfg::P2 + q]);
+          c3 = clock64();
+          int on = 0;
+          if (ci < N && cj < N) {
+            const double dr = Dv[ci], ds = Dv[cj];
+            const RotCoef<T> p = rot_coef<T>(acc, dr, ds, Jv[ci] == Jv[cj], otol2);
+            on = p.code == 1;
+            k_cs[q] = p.cs;
+            k_hs[q] = p.hs;
+            k_cp[q] = p.cp;
+            k_sp[q] = p.sp;
+            if (p.code < 0) atomicMin(&s_fail, ci * 4096 + cj);
+            // the D update (_kernels.py:80-81) is finished at the start of
+            // the next round, off the critical path
+            pd_on = on;
+            pd_ci = ci;
+            pd_cj = cj;
+            pd_dr = dr;
+            pd_ds = ds;
+            pd_num = p.num;
+            pd_den = p.den;
+            pd_eta = p.eta;
+            pd_hyp = p.hyp;
+          }
+          k_on[q] = on;
+          c4 = clock64();
+        }
+        __syncthreads();
+        if constexpr (C > 1) {
+          // this round's buffer is consumed: re-arm it for round gr+2 before
+          // the end-of-round barrier, i.e. before this CTA pushes round gr+1
+          // (no peer can push round gr+2 into it earlier)
+          if (tid == NT - 1) mbar_arm(&s_mbar[buf], TX);
+        }
+        const long long c5 = clock64();
+        // (3) slab phase: apply, then the ring step
+        if (in_ring && k_on[slot]) {
+          RotCoef<T> p;
+          p.cs = k_cs[slot];
+          p.hs = k_hs[slot];
+          p.cp = k_cp[slot];
+          p.sp = k_sp[slot];
+#pragma unroll
+          for (int u = 0; u < RPT; ++u) rot_fold<T>(X[u], Y[u], p);
+        }
+        // ---- ring step: strategies.py:75-92 (nbl = ne) ----
+        const bool send_i = ip + jp > ne;
+        if (send_i) {
+          ++ip;
+          if (ip == jp) {
+            ip -= pr;
+            jp = ip;
+          }
+          ib = ip;
+        } else {
+          ++jp;
+          jb = jp;
+        }
+        // odd sweeps: receive from slot+1, send to slot-1 (strategies.py:69-72)
+        const int par = gr & 1;
+        const bool via_smem = odd ? (wslot == SPW - 1 || slot == pr - 1) : (wslot == 0 || slot == 0);
+        const bool writer = in_ring && (odd ? (wslot == 0) : (wslot == SPW - 1 || slot == pr - 1));
+        const int src = odd ? (slot + 1 == pr ? 0 : slot + 1) : (slot == 0 ? pr - 1 : slot - 1);
+        T *xw = xbuf + (size_t(par) * Cfg::NWARP + warp) * RPC;
+        const T *xr = xbuf + (size_t(par) * Cfg::NWARP + src / SPW) * RPC;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const T v = send_i ? X[u] : Y[u];
+          if (writer) xw[lane_in + u * TPP] = v;
+          const T nv = odd ? shfl_down(v, TPP) : shfl_up(v, TPP);
+          if (send_i)
+            X[u] = nv;
+          else
+            Y[u] = nv;
+        }
+        if (in_ring && lane_in == 0) {
+          cib[slot] = ib - 1;
+          cjb[slot] = jb - 1;
+        }
+        const long long c6 = clock64();
+        __syncthreads();
+        const long long c7 = clock64();
+        if (in_ring && via_smem) {
+#pragma unroll
+          for (int u = 0; u < RPT; ++u) {
+            const T nv = xr[lane_in + u * TPP];
+            if (send_i)
+              X[u] = nv;
+            else
+              Y[u] = nv;
+          }
+        }
+        const long long c8 = clock64();
+        if (a.prof) {
+          ph[0] += c1 - c0; ph[1] += c2 - c1; ph[2] += c3 - c2; ph[3] += c4 - c3;
+          ph[4] += c5 - c4; ph[5] += c6 - c5; ph[6] += c7 - c6; ph[7] += c8 - c7;
+        }
         if (s_fail != INT_MAX) break;
       }
+      if (pd_on) finish_d();
+      if (my_cnt) atomicAdd(&s_cnt[sw & 1], my_cnt);
+      nrot_total += 0;
+      my_cnt = 0;
+      __syncthreads();
       if (s_fail != INT_MAX) {
         status = PV_INDEFINITE;
         break;
@@ -448,22 +649,98 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       if (cnt == 0) break;
     }
   }
+  t_jac = clock64();
+
+  // ------------------------------------------------------------------ W = R0^-1 R
+  // R_final columns -> shared slab Fs (by column); back substitution by row
+  // blocks from the last CTA of the cluster to the first.
+  T *Fs = Ws;  // RPC x NMAX slab (scratch region is large enough)
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    if (!in_ring) break;
+    const int row = lane_in + u * TPP;
+    Fs[(ib - 1) * RS + row] = X[u];
+    Fs[(jb - 1) * RS + row] = Y[u];
+  }
+  if (my_big) atomicAdd(&s_big, my_big);
+  if (my_maxt > 0.0) atomicMax(&s_maxt, static_cast<unsigned long long>(__double_as_longlong(my_maxt)));
+  __syncthreads();
+  for (int k = C - 1; k >= 0; --k) {
+    if (crank == k) {
+      // local rows, last to first; columns of W are independent, so each
+      // thread back-substitutes whole columns (no barrier inside the block)
+      for (int c = tid; c < N; c += NT) {
+        for (int gl = RPC - 1; gl >= 0; --gl) {
+          const int g = row0 + gl;
+          if (g >= N) continue;
+          const T w = divr(Fs[c * RS + gl], re(Rs[g * RS + gl]));
+          Fs[c * RS + gl] = w;
+          for (int gl2 = 0; gl2 < gl; ++gl2) Fs[c * RS + gl2] = sub(Fs[c * RS + gl2], mul(Rs[g * RS + gl2], w));
+        }
+      }
+      __syncthreads();
+    }
+    cluster_sync<C>();
+    if (crank < k) {
+      // T[rows of this CTA] -= R0[these rows, block k] W[block k, :]; the
+      // block of W is first copied from CTA k (DSMEM) into local scratch
+      const T *Wk = remote<C>(Fs, k);
+      T *Wl = part;  // scratch (>= RPC * NMAX elements, see PivCfg)
+      const int rk0 = k * RPC;
+      for (int e = tid; e < RPC * N; e += NT) {
+        const int j = e % RPC, c = e / RPC;
+        Wl[j * NMAX + c] = Wk[c * RS + j];
+      }
+      __syncthreads();
+      const int jn = min(RPC, N - rk0);
+      for (int e = tid; e < RPC * N; e += NT) {
+        const int gl = e % RPC, c = e / RPC;
+        if (row0 + gl >= N) continue;
+        T acc = Fs[c * RS + gl];
+        for (int j = 0; j < jn; ++j) acc = sub(acc, mul(Rs[(rk0 + j) * RS + gl], Wl[j * NMAX + c]));
+        Fs[c * RS + gl] = acc;
+      }
+    }
+    cluster_sync<C>();
+  }
 
   // ------------------------------------------------------------------ out
-  const int nmax = a.nmax;
-  T *Wout = reinterpret_cast<T *>(a.W) + int64_t(item_id) * nmax * nmax;
-  for (int e = tid; e < RPC * N; e += NT) {
-    const int gl = e % RPC, c = e / RPC;
-    const int g = row0 + gl;
-    if (g < N) Wout[g + int64_t(c) * nmax] = Ws[gl + c * RS];
-  }
-  if (a.Rout) {
-    T *Rout = reinterpret_cast<T *>(a.Rout) + int64_t(item_id) * nmax * nmax;
+  {
+    const int nmax = a.nmax;
+    T *Wout = reinterpret_cast<T *>(a.W) + int64_t(item_id) * nmax * nmax;
+    T *Rout = a.Rout ? reinterpret_cast<T *>(a.Rout) + int64_t(item_id) * nmax * nmax : nullptr;
     for (int e = tid; e < RPC * N; e += NT) {
       const int gl = e % RPC, c = e / RPC;
       const int g = row0 + gl;
-      if (g < N) Rout[g + int64_t(c) * nmax] = Rs[gl + c * RS];
+      if (g < N) Wout[g + int64_t(c) * nmax] = Fs[c * RS + gl];
     }
+    if (Rout) {
+      // R_final = R0 W (rows of this CTA), recomputed for the optional output
+      for (int e = tid; e < RPC * N; e += NT) {
+        const int gl = e % RPC, c = e / RPC;
+        const int g = row0 + gl;
+        if (g >= N) continue;
+        T acc = S<T>::zero();
+        for (int j = g; j < N; ++j) {
+          const T *Wj = remote<C>(Fs, j / RPC);
+          acc = add(acc, mul(Rs[j * RS + gl], Wj[c * RS + (j % RPC)]));
+        }
+        Rout[g + int64_t(c) * nmax] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  if (a.prof && tid == 0) {
+    long long *pf = a.prof + int64_t(blockIdx.x) * 8;
+    pf[0] = t_chol - t_start;
+    pf[1] = t_jac - t_chol;
+    pf[2] = clock64() - t_jac;
+    pf[3] = gr;
+    pf[4] = sweeps;
+    pf[5] = fallback;
+    long long *pp = a.prof + int64_t(gridDim.x) * 8 + int64_t(blockIdx.x) * 8;
+    for (int i = 0; i < 8; ++i) pp[i] = ph[i];
   }
   if (crank == 0 && tid == 0) {
     int64_t *st = a.stats + int64_t(item_id) * ST_N;
@@ -477,7 +754,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     st[ST_FALLBACK] = fallback;
   }
   // keep every CTA's shared memory alive until remote readers are done
-  if constexpr (C > 1) cg::this_cluster().sync();
+  cluster_sync<C>();
 }
 
 template <typename T, int NMAX, int C, int NT>
@@ -518,50 +795,91 @@ int pivot_nmax(int bmax) {
   return -1;
 }
 
-int pivot_default_cluster(bool cx, int nmax) {
-  // R and W slabs <= ~140 KB of shared memory per CTA
-  const size_t bytes = 2ull * nmax * nmax * (cx ? 16 : 8);
+static size_t pivot_smem(bool cx, int nmax, int c) {
+  const size_t w = cx ? 16 : 8;
+  const size_t rs = nmax / c + 1;
+  const size_t slab = nmax * rs;
+  return (slab + std::max<size_t>(slab, 16 * nmax)) * w + 2 * c * (nmax / 2) * w + 2 * nmax * w +
+         3 * nmax * 8 + nmax * 4;
+}
+
+int pivot_default_cluster(bool cx, int nmax, int count) {
+  // smallest cluster whose shared-memory slabs fit ...
   int c = 1;
-  while (bytes / c > 140 * 1024) c *= 2;
+  while (c < 16 && pivot_smem(cx, nmax, c) > 200 * 1024) c *= 2;
+  // ... then spread each pivot over more SMs until the batch gives ~2 CTAs
+  // per SM (148 SMs), so the latency chains of two pivots interleave, while
+  // every CTA keeps >= 8 rows
+  while (c < 4 && nmax / (2 * c) >= 8 && nmax / (2 * c) >= 512 / nmax && count * 2 * c <= 148) c *= 2;
   return c;
 }
 
-template <typename T, int NMAX, int C>
+template <typename T, int NMAX, int C, int NT>
 static cudaError_t launch_if_valid(const PivotArgs &a, cudaStream_t st) {
-  if constexpr (NMAX / C >= 16 && NMAX / C >= 256 / (NMAX / 2) ) {
-    if constexpr (PivCfg<T, NMAX, C, 256>::SMEM <= 227 * 1024) return launch_pivot_t<T, NMAX, C, 256>(a, st);
+  constexpr int P2 = NMAX / 2, RPC = NMAX / C;
+  if constexpr (RPC >= 4 && NT >= P2 && NT / P2 <= 32 && NT / P2 <= RPC && NT <= RPC * NMAX) {
+    if constexpr (PivCfg<T, NMAX, C, NT>::SMEM <= 227 * 1024) return launch_pivot_t<T, NMAX, C, NT>(a, st);
+  }
+  return cudaErrorInvalidConfiguration;
+}
+
+template <typename T, int NMAX, int C>
+static cudaError_t dispatch_nt(const PivotArgs &a, int nt, cudaStream_t st) {
+  switch (nt) {
+    case 256: return launch_if_valid<T, NMAX, C, 256>(a, st);
+    case 512: return launch_if_valid<T, NMAX, C, 512>(a, st);
+    case 1024: return launch_if_valid<T, NMAX, C, 1024>(a, st);
   }
   return cudaErrorInvalidConfiguration;
 }
 
 template <typename T, int NMAX>
-static cudaError_t dispatch_c(const PivotArgs &a, int c, cudaStream_t st) {
+static cudaError_t dispatch_c(const PivotArgs &a, int c, int nt, cudaStream_t st) {
   switch (c) {
-    case 1: return launch_if_valid<T, NMAX, 1>(a, st);
-    case 2: return launch_if_valid<T, NMAX, 2>(a, st);
-    case 4: return launch_if_valid<T, NMAX, 4>(a, st);
-    case 8: return launch_if_valid<T, NMAX, 8>(a, st);
-    case 16: return launch_if_valid<T, NMAX, 16>(a, st);
+    case 1: return dispatch_nt<T, NMAX, 1>(a, nt, st);
+    case 2: return dispatch_nt<T, NMAX, 2>(a, nt, st);
+    case 4: return dispatch_nt<T, NMAX, 4>(a, nt, st);
+    case 8: return dispatch_nt<T, NMAX, 8>(a, nt, st);
+    case 16: return dispatch_nt<T, NMAX, 16>(a, nt, st);
   }
   return cudaErrorInvalidConfiguration;
 }
 
+static int g_tune_threads = 0, g_tune_cluster = 0;
+void pivot_tune(int threads, int cluster) {
+  g_tune_threads = threads;
+  g_tune_cluster = cluster;
+}
+
+int pivot_default_threads(bool cx, int nmax, int c) {
+  // smallest CTA whose register-resident slab (4 arrays x RPT rows) stays
+  // within ~4 complex / 8 real rows per thread
+  const int p2 = nmax / 2, rpc = nmax / c, cap = cx ? 4 : 8;
+  for (int nt = 256; nt <= 1024; nt *= 2) {
+    const int tpp = nt / p2;
+    if (tpp < 1 || tpp > 32 || tpp > rpc) continue;
+    if (rpc / tpp <= cap) return nt;
+  }
+  return 1024;
+}
+
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used) {
-  const int c = cluster > 0 ? cluster : pivot_default_cluster(cx, a.nmax);
+  int c = cluster > 0 ? cluster : (g_tune_cluster > 0 ? g_tune_cluster : pivot_default_cluster(cx, a.nmax, a.count));
+  const int nt = g_tune_threads > 0 ? g_tune_threads : pivot_default_threads(cx, a.nmax, c);
   if (cluster_used) *cluster_used = c;
   if (cx) {
     switch (a.nmax) {
-      case 32: return dispatch_c<cplx, 32>(a, c, st);
-      case 64: return dispatch_c<cplx, 64>(a, c, st);
-      case 128: return dispatch_c<cplx, 128>(a, c, st);
-      case 256: return dispatch_c<cplx, 256>(a, c, st);
+      case 32: return dispatch_c<cplx, 32>(a, c, nt, st);
+      case 64: return dispatch_c<cplx, 64>(a, c, nt, st);
+      case 128: return dispatch_c<cplx, 128>(a, c, nt, st);
+      case 256: return dispatch_c<cplx, 256>(a, c, nt, st);
     }
   } else {
     switch (a.nmax) {
-      case 32: return dispatch_c<double, 32>(a, c, st);
-      case 64: return dispatch_c<double, 64>(a, c, st);
-      case 128: return dispatch_c<double, 128>(a, c, st);
-      case 256: return dispatch_c<double, 256>(a, c, st);
+      case 32: return dispatch_c<double, 32>(a, c, nt, st);
+      case 64: return dispatch_c<double, 64>(a, c, nt, st);
+      case 128: return dispatch_c<double, 128>(a, c, nt, st);
+      case 256: return dispatch_c<double, 256>(a, c, nt, st);
     }
   }
   return cudaErrorInvalidValue;

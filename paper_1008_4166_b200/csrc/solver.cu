@@ -130,7 +130,7 @@ struct PhaseCtx {
   bool cx;
   int64_t m, ld;
   void *G;
-  int bmax, nmax, cluster;
+  int bmax, nmax, cluster, cluster_req;
   const int8_t *signs;
   double otol, qtol;
   int max_sweeps;
@@ -183,7 +183,7 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   pa.Rout = Rout;
   pa.nmax = c.nmax;
   int used = 0;
-  CK(launch_pivot(c.cx, pa, c.cluster, c.st, &used));
+  CK(launch_pivot(c.cx, pa, c.cluster_req, c.st, &used));
   c.cluster = used;
   if (ev) CK(cudaEventRecord(ev[2], c.st));
   UpdateArgs u{};
@@ -306,6 +306,19 @@ int hjb_comm_destroy(void *comm) {
 
 int hjb_pivot_ld(int32_t bmax) { return pivot_nmax(bmax); }
 
+static long long *g_pivot_prof = nullptr;
+// Debug: per-CTA phase clocks of subsequent hjb_pivot launches (device
+// buffer of [count*cluster][8] int64, or NULL to disable).
+int hjb_pivot_set_profile(void *prof) {
+  g_pivot_prof = static_cast<long long *>(prof);
+  return HJB_OK;
+}
+
+int hjb_tune(int32_t pivot_threads, int32_t pivot_cluster) {
+  pivot_tune(pivot_threads, pivot_cluster);
+  return HJB_OK;
+}
+
 int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   if (!pr || !res) return fail(HJB_EINVAL, "null problem/result");
   std::memset(res, 0, sizeof(*res));
@@ -425,6 +438,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   ctx.bmax = bmax;
   ctx.nmax = nmax;
   ctx.cluster = 0;
+  ctx.cluster_req = 0;
   ctx.signs = static_cast<const int8_t *>(ws.signs.p);
   ctx.otol = pr->orth_tol;
   ctx.qtol = pr->quad_tol;
@@ -642,6 +656,7 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
   pa.stats = stats;
   pa.Rout = R_out;
   pa.nmax = nmax;
+  pa.prof = g_pivot_prof;
   cudaError_t e = launch_pivot(dtype == HJB_C128, pa, cluster, st, nullptr);
   if (e == cudaErrorInvalidConfiguration) return fail(HJB_EINVAL, "hjb_pivot: unsupported cluster size");
   CK(e);
