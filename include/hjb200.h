@@ -167,6 +167,17 @@ int hjb_update(int32_t dtype, int64_t m, void *G, int64_t ldg, const int32_t *it
 
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---- */
 
+/*
+ * Block transfers of one GPU in the multi-GPU ring (host-only): GPU `rank`
+ * of `world` hosts ring workers [rank*p/world, (rank+1)*p/world); after each
+ * step the block columns exchanged with workers on other GPUs are sent or
+ * received (parallel.py:212-221; strategies.py:69-72).  out: int32
+ * [steps][max_xfers][3] = (0-based block, peer GPU, 1 = send / 0 = receive);
+ * counts: int32 [steps].  steps = sweeps * steps_per_sweep.
+ */
+int hjb_exchange_plan(int32_t strategy, int32_t p, int32_t world, int32_t rank, int32_t sweeps,
+                      int32_t max_xfers, int32_t *out, int32_t *counts);
+
 /* 128-byte NCCL unique id for rank 0 to broadcast (e.g. via torch.distributed). */
 int hjb_comm_unique_id(char out[128]);
 /* Create the communicator of this rank; *comm receives an opaque handle. */

@@ -74,6 +74,8 @@ SIGNATURES = {
     "hjb_tune": (C.c_int, [C.c_int32, C.c_int32]),
     "hjb_update": (C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hjb_exchange_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_void_p, C.c_void_p]),
     "hjb_comm_unique_id": (C.c_int, [C.c_void_p]),
     "hjb_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     "hjb_comm_destroy": (C.c_int, [C.c_void_p]),

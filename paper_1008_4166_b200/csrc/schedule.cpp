@@ -93,4 +93,21 @@ std::vector<StepPlan> RingSchedule::advance(int nsweep) {
   return plans;
 }
 
+int gpu_of_worker(int p, int world, int q) {
+  int g = int((int64_t(q) * world) / p);
+  while (g + 1 < world && workers_lo(p, world, g + 1) <= q) ++g;
+  while (g > 0 && workers_lo(p, world, g) > q) --g;
+  return g;
+}
+
+void step_transfers(const std::vector<StepPlan> &plans, int p, int world, int rank, std::vector<Xfer> &out) {
+  const int lo = workers_lo(p, world, rank), hi = workers_lo(p, world, rank + 1);
+  for (int q = lo; q < hi; ++q) {
+    const int gs = gpu_of_worker(p, world, plans[q].snd_rnk);
+    const int gr = gpu_of_worker(p, world, plans[q].rcv_rnk);
+    if (gs != rank) out.push_back(Xfer{plans[q].snd_blk - 1, gs, true});
+    if (gr != rank) out.push_back(Xfer{plans[q].rcv_blk - 1, gr, false});
+  }
+}
+
 }  // namespace hjb

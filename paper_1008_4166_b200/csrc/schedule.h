@@ -35,4 +35,19 @@ class RingSchedule {
   std::vector<State> st_;
 };
 
+// ---- several GPUs: ring ranks are split into contiguous ranges per GPU ----
+// GPU g hosts workers [workers_lo(g), workers_lo(g+1)).
+inline int workers_lo(int p, int world, int g) { return int((int64_t(g) * p) / world); }
+int gpu_of_worker(int p, int world, int q);
+
+// One block column that crosses a GPU boundary after a step (0-based block).
+struct Xfer {
+  int blk, peer;
+  bool send;
+};
+// The transfers of GPU `rank` implied by one step's plans: worker q on this
+// GPU sends snd_blk to snd_rnk and receives rcv_blk from rcv_rnk
+// (parallel.py:212-221); only partners on another GPU need a transfer.
+void step_transfers(const std::vector<StepPlan> &plans, int p, int world, int rank, std::vector<Xfer> &out);
+
 }  // namespace hjb

@@ -270,6 +270,32 @@ int hjb_schedule(int32_t strategy, int32_t p, int32_t sweeps, int32_t *layouts, 
   return HJB_OK;
 }
 
+int hjb_exchange_plan(int32_t strategy, int32_t p, int32_t world, int32_t rank, int32_t sweeps,
+                      int32_t max_xfers, int32_t *out, int32_t *counts) {
+  if (p < 1 || world < 1 || rank < 0 || rank >= world || p < world || sweeps < 0 || max_xfers < 1 || !out || !counts)
+    return fail(HJB_EINVAL, "hjb_exchange_plan: invalid argument");
+  try {
+    RingSchedule rs(strategy, p);
+    int64_t step = 0;
+    for (int sw = 1; sw <= sweeps; ++sw)
+      for (int s = 0; s < rs.steps_per_sweep(); ++s, ++step) {
+        std::vector<Xfer> xf;
+        step_transfers(rs.advance(sw), p, world, rank, xf);
+        if (int(xf.size()) > max_xfers) return fail(HJB_EINVAL, "hjb_exchange_plan: max_xfers too small");
+        counts[step] = int32_t(xf.size());
+        for (size_t t = 0; t < xf.size(); ++t) {
+          int32_t *o = out + (step * max_xfers + int64_t(t)) * 3;
+          o[0] = xf[t].blk;
+          o[1] = xf[t].peer;
+          o[2] = xf[t].send ? 1 : 0;
+        }
+      }
+  } catch (const std::exception &e) {
+    return fail(HJB_EINVAL, e.what());
+  }
+  return HJB_OK;
+}
+
 int hjb_comm_unique_id(char out[128]) {
   ncclUniqueId id;
   NK(ncclGetUniqueId(&id));
@@ -371,18 +397,11 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   // ---- schedule -> per-sweep item tables of this GPU's workers ----
   RingSchedule ring(pr->strategy, P);
   const int steps = ring.steps_per_sweep();
-  auto wlo = [&](int g) { return int((int64_t(g) * P) / world); };
-  auto gpu_of = [&](int q) {
-    int g = int((int64_t(q) * world) / P);
-    while (g + 1 < world && wlo(g + 1) <= q) ++g;
-    while (g > 0 && wlo(g) > q) --g;
-    return g;
-  };
-  const int q_lo = wlo(grank), q_hi = wlo(grank + 1), nloc = q_hi - q_lo;
+  auto gpu_of = [&](int q) { return gpu_of_worker(P, world, q); };
+  const int q_lo = workers_lo(P, world, grank), q_hi = workers_lo(P, world, grank + 1), nloc = q_hi - q_lo;
   // layouts for max_sweeps sweeps: [sweep][1 + steps][nloc or 2*nloc]
   const int per_sweep_items = 2 * nloc + steps * nloc;
   std::vector<Item> items(size_t(pr->max_sweeps) * per_sweep_items);
-  struct Xfer { int blk, peer; bool send; };
   std::vector<std::vector<Xfer>> xfers(size_t(pr->max_sweeps) * steps);
   try {
     for (int sw = 1; sw <= pr->max_sweeps; ++sw) {
@@ -399,12 +418,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
           row[q - q_lo] = Item{part.off[bi], part.width[bi], part.off[bj], part.width[bj]};
         }
         std::vector<StepPlan> pl = ring.advance(sw);
-        auto &xf = xfers[size_t(sw - 1) * steps + s];
-        for (int q = q_lo; q < q_hi; ++q) {
-          const int gs = gpu_of(pl[q].snd_rnk), gr = gpu_of(pl[q].rcv_rnk);
-          if (gs != grank) xf.push_back(Xfer{pl[q].snd_blk - 1, gs, true});
-          if (gr != grank) xf.push_back(Xfer{pl[q].rcv_blk - 1, gr, false});
-        }
+        step_transfers(pl, P, world, grank, xfers[size_t(sw - 1) * steps + s]);
       }
     }
   } catch (const std::exception &e) {

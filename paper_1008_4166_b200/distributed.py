@@ -28,21 +28,18 @@ def gpu_of_worker(p: int, world: int, q: int) -> int:
     raise ValueError(q)
 
 
-def exchange_plan(strategy: str, p: int, world: int, sweeps: int = 1):
-    """Per step, the block transfers that cross a GPU boundary: list of
-    (src_gpu, dst_gpu, block) derived from the reference's StepPlans
-    (strategies.py:75-136).  Everything else is an index remap."""
-    from .strategies import schedule_arrays
-    _, plans = schedule_arrays(strategy, p, sweeps)
-    out = []
-    for step in plans:
-        xf = []
-        for q, (snd_rnk, snd_blk, rcv_rnk, rcv_blk) in enumerate(step):
-            src, dst = gpu_of_worker(p, world, q), gpu_of_worker(p, world, int(snd_rnk))
-            if src != dst:
-                xf.append((src, dst, int(snd_blk)))
-        out.append(xf)
-    return out
+def exchange_plan(strategy: str, p: int, world: int, rank: int, sweeps: int = 1):
+    """The native multi-GPU transfer plan of GPU ``rank`` (hjb_exchange_plan,
+    the same code hjb_solve runs): per step a list of (0-based block, peer,
+    send?) for the block columns that cross a GPU boundary."""
+    from .strategies import steps_per_sweep, strategy_code
+    steps = steps_per_sweep(strategy, p) * sweeps
+    mx = 2 * p
+    out = np.zeros((max(steps, 1), mx, 3), np.int32)
+    cnt = np.zeros(max(steps, 1), np.int32)
+    _lib.check(_lib.lib().hjb_exchange_plan(strategy_code(strategy), p, world, rank, sweeps, mx,
+                                            out.ctypes.data, cnt.ctypes.data))
+    return [[(int(b), int(pe), bool(sd)) for b, pe, sd in out[s, :cnt[s]]] for s in range(steps)]
 
 
 class Comm:
