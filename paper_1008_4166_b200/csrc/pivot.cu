@@ -36,6 +36,16 @@
 
 namespace cg = cooperative_groups;
 
+// per-round phase clocks (tools/pivot_bench.py); off in production builds
+#ifndef HJB_ROUND_PROFILE
+#define HJB_ROUND_PROFILE 0
+#endif
+#if HJB_ROUND_PROFILE
+#define RCLK() clock64()
+#else
+#define RCLK() 0LL
+#endif
+
 namespace hjb {
 
 constexpr double kEps = 2.220446049250313e-16;
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     lam[c] = (!dense && c < N) ? a.D[int64_t(item_id) * 2 * bmax + (c < ni ? c : bmax + (c - ni))] : 1.0;
   }
   for (int e = tid; e < NMAX * RS; e += NT) Rs[e] = S<T>::zero();
-  if (tid == 0) { s_fail = INT_MAX; s_maxt = 0ull; s_big = 0; s_cnt[0] = s_cnt[1] = 0; }
+  if (tid == 0) { s_fail = INT_MAX; s_maxt = 0ull; s_big = 0; s_cnt[0] = s_cnt[1] = 0; s_flag[0] = 1; }
   __syncthreads();
 
   // ------------------------------------------------------------------ R
@@ -335,35 +345,58 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   }
 
   // distributed right-looking Cholesky of rows [k0, N) of the slab, upper
+  // distributed right-looking Cholesky of rows [kstart, N) of the slab,
+  // blocked by CTA: the owner of a row block factors it locally (CTA
+  // barriers only), the cluster synchronises once per block, and every later
+  // CTA copies the finished block (DSMEM) and applies the rank-RPC update
   auto cholesky = [&](int kstart) -> bool {
-    for (int k = kstart; k < N; ++k) {
-      const int owner = k / RPC, lk = k % RPC, buf = k & 1;
-      if (crank == owner) {
-        const double d = re(Rs[lk + k * RS]);
-        const bool ok = finite_pos(d);
-        const double rkk = ok ? sqrt(d) : 1.0;
-        __syncthreads();
-        for (int l = k + tid; l < N; l += NT) {
-          const T v = (l == k) ? scale(S<T>::one(), rkk) : divr(Rs[lk + l * RS], rkk);
-          Rs[lk + l * RS] = v;
-#pragma unroll 1
-          for (int q = 0; q < C; ++q) remote<C>(rowbuf, q)[buf * NMAX + l] = v;
-        }
-        if (tid == 0) {
-#pragma unroll 1
-          for (int q = 0; q < C; ++q) remote<C>(s_flag, q)[buf] = ok ? 1 : 0;
+    for (int K = 0; K < C; ++K) {
+      const int kb0 = max(kstart, K * RPC), kb1 = min(N, (K + 1) * RPC);
+      if (kb0 >= kb1) continue;
+      if (crank == K) {
+        for (int k = kb0; k < kb1; ++k) {
+          const int lk = k - row0;
+          const double d = re(Rs[lk + k * RS]);
+          const bool ok = finite_pos(d);
+          __syncthreads();
+          if (!ok) {
+            if (tid == 0) s_flag[0] = 0;
+            break;
+          }
+          const double rkk = sqrt(d);
+          for (int l = k + tid; l < N; l += NT)
+            Rs[lk + l * RS] = (l == k) ? scale(S<T>::one(), rkk) : divr(Rs[lk + l * RS], rkk);
+          __syncthreads();
+          for (int e = tid; e < RPC * NMAX; e += NT) {
+            const int gl = e % RPC, l = e / RPC;
+            const int g = row0 + gl;
+            if (g <= k || g >= kb1 || l < g || l >= N) continue;
+            Rs[gl + l * RS] = cfms(Rs[lk + g * RS], Rs[lk + l * RS], Rs[gl + l * RS]);
+          }
+          __syncthreads();
         }
       }
       cluster_sync<C>();
-      if (!s_flag[buf]) return false;
-      const T *row = rowbuf + buf * NMAX;
-      for (int e = tid; e < RPC * NMAX; e += NT) {
-        const int gl = e % RPC, l = e / RPC;
-        const int g = row0 + gl;
-        if (g <= k || g >= N || l < g || l >= N) continue;
-        Rs[gl + l * RS] = cfms(row[g], row[l], Rs[gl + l * RS]);
+      if (!remote<C>(s_flag, K)[0]) return false;
+      if (crank > K) {
+        const T *RK = remote<C>(Rs, K);
+        T *Bl = Ws;  // scratch: (kb1-kb0) x NMAX rows of the finished block
+        const int nb = kb1 - kb0;
+        for (int e = tid; e < nb * NMAX; e += NT) {
+          const int kk = e % nb, l = e / nb;
+          Bl[kk * NMAX + l] = (l >= kb0 && l < N) ? RK[(kb0 + kk - K * RPC) + l * RS] : S<T>::zero();
+        }
+        __syncthreads();
+        for (int e = tid; e < RPC * NMAX; e += NT) {
+          const int gl = e % RPC, l = e / RPC;
+          const int g = row0 + gl;
+          if (g >= N || l < g || l >= N) continue;
+          T acc = Rs[gl + l * RS];
+          for (int kk = 0; kk < nb; ++kk) acc = cfms(Bl[kk * NMAX + g], Bl[kk * NMAX + l], acc);
+          Rs[gl + l * RS] = acc;
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
     return true;
   };
@@ -380,6 +413,8 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   }
   if (need_dense && status == PV_OK) {
     // dense fallback: chol(gram([G_i G_j])) from G itself (parallel.py:196-198)
+    cluster_sync<C>();  // every CTA is done reading the failed attempt's flag
+    if (tid == 0) s_flag[0] = 1;
     for (int e = tid; e < NMAX * RS; e += NT) Rs[e] = S<T>::zero();
     __syncthreads();
     for (int e = tid; e < RPC * NMAX; e += NT) {
@@ -493,7 +528,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       __syncthreads();
 
       for (int rnd = 0; rnd < ne; ++rnd, ++gr) {
-        const long long c0 = clock64();
+        const long long c0 = RCLK();
         if (pd_on) finish_d();
         // (1) slab phase: CTA-partial of g_i^H g_j for this slot's pair
         T d0 = S<T>::zero(), d1 = S<T>::zero();
@@ -523,7 +558,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
             if (lane_in == 0) *mine = dot;
           }
         }
-        const long long c1 = clock64();
+        const long long c1 = RCLK();
         long long c2 = c1, c3 = c1, c4 = c1;
         __syncthreads();
         // (2) pair phase: one thread per pair sums the cluster partials in
@@ -533,11 +568,11 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           const int q = tid;
           const int ci = cib[q], cj = cjb[q];
           if constexpr (C > 1) mbar_wait(&s_mbar[buf], (gr >> 1) & 1);
-          c2 = clock64();
+          c2 = RCLK();
           T acc = part[(buf * C) * Cfg::P2 + q];
 #pragma unroll 1
           for (int r = 1; r < C; ++r) acc = add(acc, part[(buf * C + r) * Cfg::P2 + q]);
-          c3 = clock64();
+          c3 = RCLK();
           int on = 0;
           if (ci < N && cj < N) {
             const double dr = Dv[ci], ds = Dv[cj];
@@ -561,7 +596,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
             pd_hyp = p.hyp;
           }
           k_on[q] = on;
-          c4 = clock64();
+          c4 = RCLK();
         }
         __syncthreads();
         if constexpr (C > 1) {
@@ -570,7 +605,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           // (no peer can push round gr+2 into it earlier)
           if (tid == NT - 1) mbar_arm(&s_mbar[buf], TX);
         }
-        const long long c5 = clock64();
+        const long long c5 = RCLK();
         // (3) slab phase: apply, then the ring step
         if (in_ring && k_on[slot]) {
           RotCoef<T> p;
@@ -601,11 +636,13 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         const int src = odd ? (slot + 1 == pr ? 0 : slot + 1) : (slot == 0 ? pr - 1 : slot - 1);
         T *xw = xbuf + (size_t(par) * Cfg::NWARP + warp) * RPC;
         const T *xr = xbuf + (size_t(par) * Cfg::NWARP + src / SPW) * RPC;
+        const int lane = threadIdx.x & 31;
+        const int src_lane = odd ? min(lane + TPP, 31) : max(lane - TPP, 0);
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
           const T v = send_i ? X[u] : Y[u];
           if (writer) xw[lane_in + u * TPP] = v;
-          const T nv = odd ? shfl_down(v, TPP) : shfl_up(v, TPP);
+          const T nv = shfl_idx(v, src_lane);
           if (send_i)
             X[u] = nv;
           else
@@ -615,9 +652,9 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           cib[slot] = ib - 1;
           cjb[slot] = jb - 1;
         }
-        const long long c6 = clock64();
+        const long long c6 = RCLK();
         __syncthreads();
-        const long long c7 = clock64();
+        const long long c7 = RCLK();
         if (in_ring && via_smem) {
 #pragma unroll
           for (int u = 0; u < RPT; ++u) {
@@ -628,8 +665,8 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
               Y[u] = nv;
           }
         }
-        const long long c8 = clock64();
-        if (a.prof) {
+        const long long c8 = RCLK();
+        if (HJB_ROUND_PROFILE && a.prof) {
           ph[0] += c1 - c0; ph[1] += c2 - c1; ph[2] += c3 - c2; ph[3] += c4 - c3;
           ph[4] += c5 - c4; ph[5] += c6 - c5; ph[6] += c7 - c6; ph[7] += c8 - c7;
         }
@@ -854,7 +891,7 @@ void pivot_tune(int threads, int cluster) {
 int pivot_default_threads(bool cx, int nmax, int c) {
   // smallest CTA whose register-resident slab (4 arrays x RPT rows) stays
   // within ~4 complex / 8 real rows per thread
-  const int p2 = nmax / 2, rpc = nmax / c, cap = cx ? 4 : 8;
+  const int p2 = nmax / 2, rpc = nmax / c, cap = 8;
   for (int nt = 256; nt <= 1024; nt *= 2) {
     const int tpp = nt / p2;
     if (tpp < 1 || tpp > 32 || tpp > rpc) continue;
