@@ -707,14 +707,25 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     if (crank == k) {
       // local rows, last to first; columns of W are independent, so each
       // thread back-substitutes whole columns (no barrier inside the block)
+      for (int gl = tid; gl < RPC; gl += NT) {
+        const int g = row0 + gl;
+        npart[gl] = g < N ? 1.0 / re(Rs[g * RS + gl]) : 0.0;  // reciprocal diagonal
+      }
+      __syncthreads();
       for (int c = tid; c < N; c += NT) {
+        T col[RPC];
+#pragma unroll
+        for (int gl = 0; gl < RPC; ++gl) col[gl] = Fs[c * RS + gl];
+#pragma unroll
         for (int gl = RPC - 1; gl >= 0; --gl) {
-          const int g = row0 + gl;
-          if (g >= N) continue;
-          const T w = divr(Fs[c * RS + gl], re(Rs[g * RS + gl]));
-          Fs[c * RS + gl] = w;
-          for (int gl2 = 0; gl2 < gl; ++gl2) Fs[c * RS + gl2] = sub(Fs[c * RS + gl2], mul(Rs[g * RS + gl2], w));
+          if (row0 + gl >= N) continue;
+          const T w = scale(col[gl], npart[gl]);
+          col[gl] = w;
+#pragma unroll
+          for (int gl2 = 0; gl2 < gl; ++gl2) col[gl2] = sub(col[gl2], mul(Rs[(row0 + gl) * RS + gl2], w));
         }
+#pragma unroll
+        for (int gl = 0; gl < RPC; ++gl) Fs[c * RS + gl] = col[gl];
       }
       __syncthreads();
     }
