@@ -156,6 +156,9 @@ int hjb_pivot_set_profile(void *prof);
 /* Tuning override for the pivot kernel: threads per CTA (256/512/1024) and
  * cluster size (1..16); 0 restores the automatic choice. */
 int hjb_tune(int32_t pivot_threads, int32_t pivot_cluster);
+/* Max co-resident clusters of the pivot kernel instance for (dtype, bmax,
+ * cluster, threads) on the current device (negative: cudaError). */
+int hjb_pivot_occupancy(int32_t dtype, int32_t bmax, int32_t cluster, int32_t threads);
 
 /*
  * Block update [G_i G_j] <- [G_i G_j] W for items whose stats[0] > 0

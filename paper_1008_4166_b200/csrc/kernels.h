@@ -49,6 +49,7 @@ int pivot_nmax(int bmax);   // NMAX instance for a block width
 int pivot_default_cluster(bool cx, int nmax, int count);
 int pivot_default_threads(bool cx, int nmax, int cluster);
 void pivot_tune(int threads, int cluster);  // 0 = automatic
+int pivot_max_active_clusters(bool cx, int nmax, int cluster, int threads);
 
 struct UpdateArgs {
   void *G;

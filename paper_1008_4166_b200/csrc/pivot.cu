@@ -49,6 +49,7 @@ namespace cg = cooperative_groups;
 namespace hjb {
 
 constexpr double kEps = 2.220446049250313e-16;
+static int g_tune_threads = 0, g_tune_cluster = 0;  // hjb_tune overrides (0 = auto)
 
 template <typename T, int NMAX, int C, int NT>
 struct PivCfg {
@@ -852,23 +853,78 @@ static size_t pivot_smem(bool cx, int nmax, int c) {
 }
 
 int pivot_default_cluster(bool cx, int nmax, int count) {
-  // smallest cluster whose shared-memory slabs fit ...
-  int c = 1;
-  while (c < 16 && pivot_smem(cx, nmax, c) > 200 * 1024) c *= 2;
-  // ... then spread each pivot over more SMs until the batch gives ~2 CTAs
-  // per SM (148 SMs), so the latency chains of two pivots interleave, while
-  // every CTA keeps >= 8 rows
-  while (c < 4 && nmax / (2 * c) >= 8 && nmax / (2 * c) >= 512 / nmax && count * 2 * c <= 148) c *= 2;
-  return c;
+  // smallest cluster whose shared-memory slabs fit
+  int cmin = 1;
+  while (cmin < 16 && pivot_smem(cx, nmax, cmin) > 200 * 1024) cmin *= 2;
+  // largest cluster (rows per CTA >= 16) whose whole batch is co-resident in
+  // one wave (cudaOccupancyMaxActiveClusters: e.g. 33 clusters of 4 but only
+  // 15 of 8 on a 148-SM B200); if none, the batch needs several waves anyway
+  // and the smallest cluster has the least exchange overhead
+  static int cache[2][5][5];
+  const int ni = nmax == 32 ? 0 : nmax == 64 ? 1 : nmax == 128 ? 2 : 3;
+  int best = cmin;
+  for (int c = cmin; c <= 16; c *= 2) {
+    if (nmax / c < 16 && c > cmin) break;
+    const int ci = c == 1 ? 0 : c == 2 ? 1 : c == 4 ? 2 : c == 8 ? 3 : 4;
+    const int nt = pivot_default_threads(cx, nmax, c);
+    int &occ = cache[cx][ni][ci];
+    if (occ == 0) occ = pivot_max_active_clusters(cx, nmax, c, nt);
+    if (occ >= count) best = c;
+  }
+  return best;
+}
+
+static int g_query_clusters = 0;  // when set, launch_pivot only reports max active clusters
+
+template <typename T, int NMAX, int C, int NT>
+static cudaError_t query_clusters(int *out) {
+  using Cfg = PivCfg<T, NMAX, C, NT>;
+  auto k = pivot_kernel<T, NMAX, C, NT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));
+  if (e != cudaSuccess) return e;
+  if (C > 8) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * 64);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = C;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(out, k, &cfg);
 }
 
 template <typename T, int NMAX, int C, int NT>
 static cudaError_t launch_if_valid(const PivotArgs &a, cudaStream_t st) {
   constexpr int P2 = NMAX / 2, RPC = NMAX / C;
   if constexpr (RPC >= 4 && NT >= P2 && NT / P2 <= 32 && NT / P2 <= RPC && NT <= RPC * NMAX) {
-    if constexpr (PivCfg<T, NMAX, C, NT>::SMEM <= 227 * 1024) return launch_pivot_t<T, NMAX, C, NT>(a, st);
+    if constexpr (PivCfg<T, NMAX, C, NT>::SMEM <= 227 * 1024) {
+      if (g_query_clusters) return query_clusters<T, NMAX, C, NT>(&g_query_clusters);
+      return launch_pivot_t<T, NMAX, C, NT>(a, st);
+    }
   }
   return cudaErrorInvalidConfiguration;
+}
+
+int pivot_max_active_clusters(bool cx, int nmax, int c, int nt) {
+  g_query_clusters = 1;
+  PivotArgs a{};
+  a.nmax = nmax;
+  const int saved_t = g_tune_threads, saved_c = g_tune_cluster;
+  g_tune_threads = nt;
+  g_tune_cluster = c;
+  cudaError_t e = launch_pivot(cx, a, c, nullptr, nullptr);
+  g_tune_threads = saved_t;
+  g_tune_cluster = saved_c;
+  const int r = g_query_clusters;
+  g_query_clusters = 0;
+  return e == cudaSuccess ? r : -int(e);
 }
 
 template <typename T, int NMAX, int C>
@@ -893,7 +949,6 @@ static cudaError_t dispatch_c(const PivotArgs &a, int c, int nt, cudaStream_t st
   return cudaErrorInvalidConfiguration;
 }
 
-static int g_tune_threads = 0, g_tune_cluster = 0;
 void pivot_tune(int threads, int cluster) {
   g_tune_threads = threads;
   g_tune_cluster = cluster;

@@ -340,6 +340,10 @@ int hjb_pivot_set_profile(void *prof) {
   return HJB_OK;
 }
 
+int hjb_pivot_occupancy(int32_t dtype, int32_t bmax, int32_t cluster, int32_t threads) {
+  return pivot_max_active_clusters(dtype == HJB_C128, pivot_nmax(bmax), cluster, threads);
+}
+
 int hjb_tune(int32_t pivot_threads, int32_t pivot_cluster) {
   pivot_tune(pivot_threads, pivot_cluster);
   return HJB_OK;
