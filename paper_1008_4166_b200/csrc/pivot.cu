@@ -72,7 +72,7 @@ struct PivCfg {
   static constexpr size_t OFF_R = 0;
   static constexpr size_t OFF_W = OFF_R + size_t(NMAX) * RS * sizeof(T);  // scratch
   static constexpr size_t OFF_PART = OFF_W + size_t(SCR) * sizeof(T);
-  static constexpr size_t PART = (2 * C * P2 > RPC * NMAX) ? 2 * C * P2 : RPC * NMAX;  // also W-block scratch
+  static constexpr size_t PART = (2 * C * P2 > RPC) ? 2 * C * P2 : RPC;  // also W-block scratch (column chunks)
   static constexpr size_t OFF_ROW = OFF_PART + PART * sizeof(T);
   static constexpr size_t OFF_NPART = OFF_ROW + 2 * size_t(NMAX) * sizeof(T);
   static constexpr size_t OFF_D = OFF_NPART + NMAX * sizeof(double);
@@ -735,20 +735,25 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       // T[rows of this CTA] -= R0[these rows, block k] W[block k, :]; the
       // block of W is first copied from CTA k (DSMEM) into local scratch
       const T *Wk = remote<C>(Fs, k);
-      T *Wl = part;  // scratch (>= RPC * NMAX elements, see PivCfg)
+      T *Wl = part;  // scratch: PART elements, processed in column chunks
+      constexpr int CW = int(Cfg::PART) / RPC;
       const int rk0 = k * RPC;
-      for (int e = tid; e < RPC * N; e += NT) {
-        const int j = e % RPC, c = e / RPC;
-        Wl[j * NMAX + c] = Wk[c * RS + j];
-      }
-      __syncthreads();
       const int jn = min(RPC, N - rk0);
-      for (int e = tid; e < RPC * N; e += NT) {
-        const int gl = e % RPC, c = e / RPC;
-        if (row0 + gl >= N) continue;
-        T acc = Fs[c * RS + gl];
-        for (int j = 0; j < jn; ++j) acc = sub(acc, mul(Rs[(rk0 + j) * RS + gl], Wl[j * NMAX + c]));
-        Fs[c * RS + gl] = acc;
+      for (int c0 = 0; c0 < N; c0 += CW) {
+        const int cw = min(CW, N - c0);
+        for (int e = tid; e < RPC * cw; e += NT) {
+          const int j = e % RPC, cc = e / RPC;
+          Wl[j * CW + cc] = Wk[(c0 + cc) * RS + j];
+        }
+        __syncthreads();
+        for (int e = tid; e < RPC * cw; e += NT) {
+          const int gl = e % RPC, cc = e / RPC;
+          if (row0 + gl >= N) continue;
+          T acc = Fs[(c0 + cc) * RS + gl];
+          for (int j = 0; j < jn; ++j) acc = sub(acc, mul(Rs[(rk0 + j) * RS + gl], Wl[j * CW + cc]));
+          Fs[(c0 + cc) * RS + gl] = acc;
+        }
+        __syncthreads();
       }
     }
     cluster_sync<C>();
