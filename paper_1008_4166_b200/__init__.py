@@ -16,8 +16,11 @@ from .errors import (
     SingularMatrixError,
     StructuralError,
 )
+from .factorization import (FactoredForm, accept_external_factor, factorize_hermitian_indefinite,
+                            order_by_inertia, scaled_condition)
 from .parallel import SolverConfig, parallel_jacobi
 from .rotations import DiagInfo, Tolerances, extract_eigen
+from .solve import SolveOptions, run_solver, solve_hermitian
 from .strategies import MODULUS, ROUND_ROBIN, generate_sweep_schedule, normalize_strategy, steps_per_sweep
 
 __version__ = "0.1.0"
@@ -28,4 +31,6 @@ __all__ = [
     "RankDeficiencyError", "SingularMatrixError", "SolverConfig", "StructuralError", "Tolerances",
     "as_matrix", "as_signs", "extract_eigen", "generate_sweep_schedule", "greedy_partition",
     "normalize_strategy", "num_blocks", "parallel_jacobi", "steps_per_sweep", "uniform_partition",
+    "FactoredForm", "accept_external_factor", "factorize_hermitian_indefinite", "order_by_inertia",
+    "scaled_condition", "SolveOptions", "run_solver", "solve_hermitian",
 ]

@@ -1,0 +1,124 @@
+"""Host front end: Hermitian indefinite factorisation H = G J G^* and helpers.
+
+This is the pre-processing step before the hot path,
+kept on the host like the reference's (pkg/src/hjacobi/factorization.py).
+The reference factorises with Bunch-Parlett complete pivoting
+(factorization.py:62-144); BASELINE.json's cfg4 asks for Bunch-Kaufman, which
+is what LAPACK's ?hetrf/?sytrf implement (via scipy.linalg.ldl).  Each 2x2
+pivot block is diagonalised in closed form and the columns scaled by
+sqrt(|eigenvalue|) exactly as factorization.py:131-143, so the signature ends
+up in J.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from .core import as_matrix, as_signs
+from .errors import RankDeficiencyError, SingularMatrixError
+
+
+@dataclass
+class FactoredForm:
+    """Factor pair (G, J) with row permutation P and inertia ordering P1
+    (factorization.py:20-29): (P H P^T)[i, j] == H[P[i], P[j]]."""
+
+    G: np.ndarray
+    J: np.ndarray
+    P: np.ndarray
+    P1: np.ndarray
+
+
+def _eigh2(a, b, c):
+    """Spectral decomposition of [[a, b], [conj(b), c]] with the stable
+    small-angle rotation (factorization.py:32-51)."""
+    if b == 0:
+        return float(a), float(c), np.eye(2)
+    ab = abs(b)
+    phase = b / ab
+    theta = (c - a) / (2.0 * ab)
+    sg = 1.0 if theta >= 0.0 else -1.0
+    t = sg / (abs(theta) + math.sqrt(theta * theta + 1.0))
+    cs = 1.0 / math.sqrt(1.0 + t * t)
+    sn = cs * t
+    return float(a - t * ab), float(c + t * ab), np.array([[cs * phase, sn * phase], [-sn, cs]])
+
+
+def factorize_hermitian_indefinite(H, herm_rtol=1e-10):
+    """H = G J G^* by Bunch-Kaufman (LAPACK ?hetrf via scipy.linalg.ldl)
+    followed by the 2x2 spectral scaling of factorization.py:131-143.
+
+    The L factor of scipy's ldl already absorbs the pivoting, so G satisfies
+    H = G J G^* with P = identity.  Raises SingularMatrixError on a zero
+    pivot, ValueError if H is not Hermitian.
+    """
+    from scipy.linalg import ldl
+
+    H = as_matrix(H)
+    n = H.shape[0]
+    if H.shape[1] != n:
+        raise ValueError("H must be square")
+    if n and not np.allclose(H, H.conj().T, rtol=herm_rtol, atol=herm_rtol * np.abs(H).max()):
+        raise ValueError("H is not Hermitian")
+    A = (H + H.conj().T) / 2
+    lu, d, _perm = ldl(A, lower=True, hermitian=True)
+    scale = np.abs(A).max() if n else 0.0
+    tiny = 64.0 * n * np.finfo(np.float64).eps * scale
+    G = np.array(lu, dtype=A.dtype, order="F")
+    J = np.empty(n, np.int8)
+    k = 0
+    while k < n:
+        if k + 1 < n and d[k + 1, k] != 0:
+            lam1, lam2, Q = _eigh2(d[k, k].real, d[k, k + 1], d[k + 1, k + 1].real)
+            if min(abs(lam1), abs(lam2)) <= tiny:
+                raise SingularMatrixError("zero pivot: H is numerically singular; supply a factor directly")
+            S = Q @ np.diag([math.sqrt(abs(lam1)), math.sqrt(abs(lam2))])
+            G[:, k:k + 2] = G[:, k:k + 2] @ S.astype(G.dtype)
+            J[k], J[k + 1] = (1 if lam1 >= 0 else -1), (1 if lam2 >= 0 else -1)
+            k += 2
+        else:
+            dk = d[k, k].real
+            if abs(dk) <= tiny:
+                raise SingularMatrixError("zero pivot: H is numerically singular; supply a factor directly")
+            G[:, k] *= math.sqrt(abs(dk))
+            J[k] = 1 if dk >= 0 else -1
+            k += 1
+    return FactoredForm(G=np.asfortranarray(G), J=J, P=np.arange(n), P1=np.arange(n))
+
+
+def order_by_inertia(f: FactoredForm) -> FactoredForm:
+    """Stable permutation putting +1 before -1 (factorization.py:147-153)."""
+    idx = np.argsort(f.J == -1, kind="stable")
+    return replace(f, G=np.asfortranarray(f.G[:, idx]), J=f.J[idx], P1=f.P1[idx])
+
+
+def scaled_condition(A):
+    """kappa of A scaled to unit diagonal (factorization.py:156-168);
+    diagnostic only."""
+    A = as_matrix(A)
+    d = np.diag(A).real
+    if np.any(d <= 0):
+        raise ValueError("scaled_condition requires a strictly positive diagonal")
+    s = 1.0 / np.sqrt(d)
+    As = A * np.outer(s, s)
+    w = np.abs(np.linalg.eigvalsh((As + As.conj().T) / 2))
+    return math.inf if w.min() == 0.0 else float(w.max() / w.min())
+
+
+def accept_external_factor(G, J) -> FactoredForm:
+    """Wrap a user-supplied full-column-rank factor (factorization.py:171-189)."""
+    G = as_matrix(G)
+    m_rows, n_cols = G.shape
+    if n_cols > m_rows:
+        raise ValueError("factor must have at least as many rows as columns")
+    signs = as_signs(J, n_cols)
+    try:
+        np.linalg.cholesky(G.conj().T @ G)
+    except np.linalg.LinAlgError as exc:
+        raise RankDeficiencyError("supplied factor is rank deficient") from exc
+    if n_cols and (np.abs(G) ** 2).sum(axis=0).min() == 0.0:
+        raise RankDeficiencyError("supplied factor has a zero column")
+    return FactoredForm(G=G, J=signs, P=np.arange(m_rows), P1=np.arange(n_cols))

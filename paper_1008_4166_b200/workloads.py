@@ -81,6 +81,32 @@ def cfg3(n=4096, b=64):
                     f"graded real {n}x{n}, seed 2/3, P(-1)=0.3, b={b}")
 
 
+def cfg4_hermitian(n=8192):
+    """H = Q diag(lam) Q^*: Q from QR of a complex Gaussian (seed 4),
+    lam_k = s_k 10^-v_k, v ~ U[0,6], s_k = -1 on half the indices."""
+    r = np.random.default_rng(4)
+    X = (r.standard_normal((n, n)) + 1j * r.standard_normal((n, n))) * math.sqrt(0.5)
+    Q, _ = np.linalg.qr(X)
+    v = r.uniform(0.0, 6.0, n)
+    s = np.ones(n)
+    s[r.permutation(n)[: n // 2]] = -1.0
+    lam = s * 10.0 ** (-v)
+    H = (Q * lam[None, :]) @ Q.conj().T
+    return (H + H.conj().T) / 2, lam
+
+
+def cfg4(n=8192, b=64):
+    """Prescribed spectrum, factorised on the host by Bunch-Kaufman + 2x2
+    spectral scaling (factorization.py), inertia ordered; b = 64."""
+    from .factorization import factorize_hermitian_indefinite, order_by_inertia
+    H, lam = cfg4_hermitian(n)
+    f = order_by_inertia(factorize_hermitian_indefinite(H))
+    w = Workload("cfg4", np.asfortranarray(f.G), np.ascontiguousarray(f.J), b, n // (2 * b),
+                 f"complex128 prescribed spectrum n={n}, Bunch-Kaufman factor, b={b}")
+    w.H, w.lam = H, np.sort(lam)
+    return w
+
+
 def cfg5r(n=32768, b=128):
     G = np.asfortranarray(np.random.default_rng(5).standard_normal((n, n)))
     J = np.array([1] * (n // 2) + [-1] * (n - n // 2), np.int8)
@@ -98,7 +124,7 @@ def cfg5c(n=16384, b=128):
                     f"complex128 {n}x{n} seed 6, J half/half, b={b}")
 
 
-CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg5r": cfg5r, "cfg5c": cfg5c}
+CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5r": cfg5r, "cfg5c": cfg5c}
 
 
 def make(name: str, **kw) -> Workload:

@@ -136,6 +136,8 @@ def config_proxies():
         ("cfg2", {"n": 512, "b": 32}),
         ("cfg3", {"n": 512, "b": 32}),
         ("cfg5r", {"n": 512, "b": 64}),
+        ("cfg5r", {"n": 1024, "b": 128}),
+        ("cfg5c", {"n": 1024, "b": 128}),
     ]
     meta = {}
     for name, kw in runs:

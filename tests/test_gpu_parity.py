@@ -248,7 +248,8 @@ def test_cfg1_full_size(pkg):
 
 
 @pytest.mark.parametrize("name,kw", [("cfg2", {"n": 512, "b": 32}), ("cfg3", {"n": 512, "b": 32}),
-                                     ("cfg5r", {"n": 512, "b": 64})])
+                                     ("cfg5r", {"n": 512, "b": 64}), ("cfg5r", {"n": 1024, "b": 128}),
+                                     ("cfg5c", {"n": 1024, "b": 128})])
 def test_config_proxies(pkg, name, kw):
     from paper_1008_4166_b200 import workloads
 
@@ -321,3 +322,22 @@ def test_cluster_sizes_agree(pkg, torch):
             if not cplx:
                 assert np.max(np.abs(W[0][0] - outs[0][0][0])) <= 1e-10 * np.abs(outs[0][0][0]).max()
             assert np.max(np.abs(lam - lams[0]) / np.abs(lams[0])) <= 1e-12
+
+
+def test_cfg4_proxy_solve_hermitian_known_spectrum(pkg):
+    """cfg4 at n = 256 through the drop-in solve_hermitian: Bunch-Kaufman on
+    the host, 2F ring on the GPU, extraction on the GPU; the spectrum is known
+    by construction (the reference's criterion 3 pattern,
+    test_acceptance.py:107-137)."""
+    from paper_1008_4166_b200 import workloads
+
+    w = workloads.cfg4(n=256, b=16)
+    opts = pkg.SolveOptions(variant="2F", strategy="round_robin", p=w.p,
+                            tol=pkg.Tolerances(orth_tol=w.n * EPS))
+    res, metrics = pkg.solve_hermitian(w.H, opts)
+    lam = np.sort(res.eigenvalues)
+    kappa = math.sqrt(metrics["scaled_condition"])
+    assert res.converged
+    assert np.all(np.abs(lam - w.lam) <= 64 * w.n * EPS * kappa * np.abs(w.lam))
+    assert metrics["orthogonality"] <= 64 * w.n * EPS
+    assert metrics["residual"] <= 64 * w.n * EPS
