@@ -241,12 +241,12 @@ cudaError_t launch_gram(bool cx, GramArgs a, cudaStream_t st) {
   a.tiles = (a.bmax + tile - 1) / tile;
   const bool v16 = cx || (a.ldg % 2 == 0);
   if (cx) {
-    if (tile == 32) return launch_gram_t<cplx, 1, 16, 3, 16>(a, st);
-    return launch_gram_t<cplx, 2, 16, 3, 16>(a, st);
+    if (tile == 32) return launch_gram_t<cplx, 1, 16, 2, 16>(a, st);
+    return launch_gram_t<cplx, 2, 16, 2, 16>(a, st);
   }
   if (tile == 32)
-    return v16 ? launch_gram_t<double, 1, 32, 3, 16>(a, st) : launch_gram_t<double, 1, 32, 3, 8>(a, st);
-  return v16 ? launch_gram_t<double, 2, 32, 3, 16>(a, st) : launch_gram_t<double, 2, 32, 3, 8>(a, st);
+    return v16 ? launch_gram_t<double, 1, 32, 2, 16>(a, st) : launch_gram_t<double, 1, 32, 2, 8>(a, st);
+  return v16 ? launch_gram_t<double, 2, 32, 2, 16>(a, st) : launch_gram_t<double, 2, 32, 2, 8>(a, st);
 }
 
 int gram_kc(bool cx) { return cx ? 16 : 32; }

@@ -874,7 +874,7 @@ int pivot_default_cluster(bool cx, int nmax, int count) {
     const int nt = pivot_default_threads(cx, nmax, c);
     int &occ = cache[cx][ni][ci];
     if (occ == 0) occ = pivot_max_active_clusters(cx, nmax, c, nt);
-    if (occ >= count) best = c;
+    if (occ >= count && (count * c <= 148 || c == cmin)) best = c;  // one wave, one CTA per SM
   }
   return best;
 }
