@@ -196,7 +196,7 @@ def main():
     dev = torch.device("cuda", local)
     comm = None
     pg = None
-    if world > 1:
+    if world > 1 or "LOCAL_RANK" in os.environ:  # torchrun: NCCL ring comm even at N=1
         import torch.distributed as dist
         dist.init_process_group("gloo", init_method="env://")
         pg = dist

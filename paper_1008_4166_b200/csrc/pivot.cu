@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   int crank = 0;
   if constexpr (C > 1) crank = int(cg::this_cluster().block_rank());
   const long long t_start = clock64();
-  long long t_chol = 0, t_jac = 0;
+  long long t_chol = 0, t_jac = 0, t_rij = 0, t_s = 0;
   const int item_id = blockIdx.x / C;
   const Item it = a.items[item_id];
   const int tid = threadIdx.x;
@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       }
       __threadfence();
       cluster_sync<C>();
+      t_rij = clock64();
       // rows g in [ni, N): S[k][l] = L_j[k] d_kl - sum_h conj(Rij[h][k]) Rij[h][l], l >= k
       T acc[OPT];
 #pragma unroll
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         Rs[gl + (ni + l) * RS] = v;
       }
       __syncthreads();
+      t_s = clock64();
       k0 = ni;
     }
   } else {
@@ -793,6 +795,8 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     pf[3] = gr;
     pf[4] = sweeps;
     pf[5] = fallback;
+    pf[6] = t_rij ? t_rij - t_start : 0;
+    pf[7] = t_s ? t_s - t_start : 0;
     long long *pp = a.prof + int64_t(gridDim.x) * 8 + int64_t(blockIdx.x) * 8;
     for (int i = 0; i < 8; ++i) pp[i] = ph[i];
   }

@@ -549,7 +549,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
           tx += ms;
         }
     }
-    if (world > 1) {  // all-reduce of the sweep's rotation count and error (parallel.py:99-118)
+    if (comm) {  // all-reduce of the sweep's rotation count and error (parallel.py:99-118)
       int64_t *rh = static_cast<int64_t *>(ws.red_h.p);
       rh[0] = rot;
       rh[1] = err != HJB_OK ? 1 : 0;
@@ -575,7 +575,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   }
 
   // ---- gather: every block from the GPU whose worker holds it ----
-  if (world > 1) {
+  if (comm) {
     std::vector<int> owner(nbl, 0);
     for (int q = 0; q < P; ++q) {
       owner[ring.i_blk(q) - 1] = gpu_of(q);

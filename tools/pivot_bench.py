@@ -67,7 +67,7 @@ for c, nt in itertools.product([int(x) for x in a.clusters.split(",")], [int(x) 
     s = stt.cpu().numpy().reshape(-1, 8)
     print(f"{w.name} b={b} cluster={c} threads={nt}: {min(ts):.3f} ms  pivots={items.shape[0]} inner sweeps avg {s[:,3].mean():.2f} max {s[:,3].max()} "
           f"rounds max {pf[:,3].max()}  chol kcyc avg {pf[:,0].mean()/1e3:.1f} max {pf[:,0].max()/1e3:.1f}  "
-          f"jacobi kcyc max {pf[:,1].max()/1e3:.1f}  cyc/round {pf[:,1].max()/max(1,pf[:,3].max()):.0f}  out kcyc {pf[:,2].max()/1e3:.1f}", flush=True)
+          f"[Rij {pf[:,6].mean()/1e3:.1f} S {pf[:,7].mean()/1e3:.1f}] jacobi kcyc max {pf[:,1].max()/1e3:.1f}  cyc/round {pf[:,1].max()/max(1,pf[:,3].max()):.0f}  out kcyc {pf[:,2].max()/1e3:.1f}", flush=True)
     R = max(1, pf[:, 3].max())
     names = ["dot+shfl", "push", "mbar", "pull+red", "params+upd", "ring shfl", "sync", "smem recv+arm"]
     print("   per-round cycles (thread 0):", "  ".join(f"{nm} {ph[:, i].mean()/R:.0f}" for i, nm in enumerate(names)), flush=True)
