@@ -14,7 +14,7 @@ import threading
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhjb200.so")
+LIB_PATH = os.environ.get("HJB_LIB") or os.path.join(HERE, "libhjb200.so")
 
 HJB_OK, HJB_EINVAL, HJB_PIVOT_INDEFINITE, HJB_CHOL_FAIL, HJB_ECUDA, HJB_ENCCL, HJB_ENOMEM = range(7)
 HJB_F64, HJB_C128 = 0, 1

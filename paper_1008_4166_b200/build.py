@@ -18,8 +18,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libhjb200.so")
-OBJ = os.path.join(ROOT, "build", "obj")
+OUT = os.environ.get("HJB_LIB") or os.path.join(HERE, "libhjb200.so")
+OBJ = os.path.join(ROOT, "build", "obj" + os.environ.get("HJB_OBJ_TAG", ""))
 SOURCES = ["schedule.cpp", "gram.cu", "pivot.cu", "update.cu", "solver.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -44,6 +44,7 @@ def _compile(src, inc, verbose):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     flags = [nvcc(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
              "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", src, "-o", obj]
+    flags += os.environ.get("HJB_NVCC_FLAGS", "").split()
     if src.endswith(".cu"):
         flags += ["--expt-relaxed-constexpr"]
         if verbose:

@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cfloat>
 #include <climits>
 
@@ -58,27 +59,42 @@ struct PivCfg {
   static constexpr int P2 = NMAX / 2;    // pair slots per round
   static constexpr int TPP = NT / P2;    // threads per pair slot
   static constexpr int RPT = RPC / TPP;  // rows per thread
-  static constexpr int OPT = RPC * NMAX / NT;  // Cholesky outputs per thread
+  static constexpr int OPT = RPC * NMAX / NT;  // Cholesky outputs per thread (distributed path)
   static constexpr int HC = 16;                // R_ij rows staged per chunk
   static_assert(TPP >= 1 && TPP <= 32 && (TPP & (TPP - 1)) == 0, "threads per pair");
   static_assert(RPT >= 1 && RPC % TPP == 0, "rows per thread");
   static_assert(OPT >= 1 && (RPC * NMAX) % NT == 0, "outputs per thread");
   static constexpr int NWARP = NT / 32;
   static constexpr int SPW = 32 / TPP;                       // pair slots per warp
-  static constexpr int XBUF = 2 * NWARP * RPC;               // [parity][warp][row]
-  static constexpr int SCR0 = HC * NMAX > XBUF ? HC * NMAX : XBUF;
-  static constexpr int SCR = SCR0 > NMAX * RS ? SCR0 : NMAX * RS;   // also the R_final / W slab
+  static constexpr int XBUF = 2 * NWARP * RPC;               // ring pass buffers [parity][warp][row]
+  // fast path: the whole b x b factor U (Schur complement / block Gram
+  // Cholesky) is kept in every CTA; register tile of the Cholesky
+  static constexpr int UB = NMAX / 2;                        // largest block width
+  static constexpr int UL = UB + 1;                          // U column stride
+  static constexpr int TI = UB < 16 ? UB : 16;               // Cholesky thread grid TI x TL
+  static constexpr int TL = NT / TI;
+  static constexpr int XI = UB / TI;                         // rows per thread
+  static constexpr int YL = (UB + TL - 1) / TL;              // columns per thread
+  static constexpr int RV = (UB + 31) / 32;                  // back-substitution rows per lane
+  static constexpr int SCR0 = HC * NMAX;
+  static constexpr int SCR1 = SCR0 > NMAX * RS ? SCR0 : NMAX * RS;  // also the R_final / W slab
+  static constexpr bool FAST_OK = NMAX <= 128 && XI * YL <= 32;
+  static constexpr int SCR = (FAST_OK && UB * UL > SCR1) ? UB * UL : SCR1;
   // shared-memory carve-up (bytes, 16-aligned)
   static constexpr size_t OFF_R = 0;
-  static constexpr size_t OFF_W = OFF_R + size_t(NMAX) * RS * sizeof(T);  // scratch
-  static constexpr size_t OFF_PART = OFF_W + size_t(SCR) * sizeof(T);
+  static constexpr size_t OFF_W = OFF_R + size_t(NMAX) * RS * sizeof(T);  // scratch / U
+  static constexpr size_t OFF_X = OFF_W + size_t(SCR) * sizeof(T);        // ring buffers
+  static constexpr size_t OFF_XD = OFF_X + size_t(XBUF) * sizeof(T);      // their D values
+  static constexpr size_t OFF_PART = OFF_XD + 2 * NWARP * sizeof(double);
   static constexpr size_t PART = (2 * C * P2 > RPC) ? 2 * C * P2 : RPC;  // also W-block scratch (column chunks)
-  static constexpr size_t OFF_ROW = OFF_PART + PART * sizeof(T);
-  static constexpr size_t OFF_NPART = OFF_ROW + 2 * size_t(NMAX) * sizeof(T);
-  static constexpr size_t OFF_D = OFF_NPART + NMAX * sizeof(double);
-  static constexpr size_t OFF_LAM = OFF_D + NMAX * sizeof(double);
+  static constexpr size_t OFF_ROW = OFF_PART + PART * sizeof(T);         // Cholesky row buffers [2][UB]
+  static constexpr size_t OFF_NPART = OFF_ROW + 2 * size_t(UB) * sizeof(T);
+  // [2][C][P2] column-norm pairs (complex: they fit the dot-partial buffer)
+  static constexpr size_t NPART = (!S<T>::cx && 4 * C * P2 > NMAX) ? 4 * C * P2 : NMAX;
+  static constexpr size_t OFF_LAM = OFF_NPART + NPART * sizeof(double);
   static constexpr size_t OFF_J = OFF_LAM + NMAX * sizeof(double);
   static constexpr size_t SMEM = OFF_J + NMAX * sizeof(int);
+  static constexpr bool FAST = FAST_OK && SMEM <= 227 * 1024;
 };
 
 // cluster-scope barrier with release/acquire semantics only (cg's sync()
@@ -108,16 +124,23 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
-__device__ __forceinline__ void mbar_arm(uint64_t *bar, unsigned tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+// wait for the phase with the given parity.  CTA-scope acquire: the data
+// guarded here is this CTA's shared memory, written by its own warps or by
+// the peers' st.async (whose bytes complete_tx on this barrier) -- a
+// cluster-scope acquire would add an L1 invalidation (CCTL.IVALL) per wait
+__device__ __forceinline__ void mbar_wait_cta(uint64_t *bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
-      "HJB_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra HJB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "HJB_WAITC_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HJB_WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
 }
@@ -134,6 +157,19 @@ __device__ __forceinline__ void st_async(uint32_t raddr, double v, uint32_t rbar
 __device__ __forceinline__ void st_async(uint32_t raddr, cplx v, uint32_t rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
                "l"(__double_as_longlong(v.x)), "l"(__double_as_longlong(v.y)), "r"(rbar)
+               : "memory");
+}
+
+// predicated shared-memory store (no branch, so the surrounding shuffles stay
+// in one basic block)
+__device__ __forceinline__ void st_shared_if(bool p, double *dst, double v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.f64 [%1], %2;\n}\n" ::"r"(int(p)),
+               "r"(smem_u32(dst)), "d"(v)
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_if(bool p, cplx *dst, cplx v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.v2.f64 [%1], {%2, %3};\n}\n" ::"r"(int(p)),
+               "r"(smem_u32(dst)), "d"(v.x), "d"(v.y)
                : "memory");
 }
 
@@ -220,9 +256,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   T *Rs = reinterpret_cast<T *>(smem + Cfg::OFF_R);
   T *Ws = reinterpret_cast<T *>(smem + Cfg::OFF_W);
   T *part = reinterpret_cast<T *>(smem + Cfg::OFF_PART);
-  T *rowbuf = reinterpret_cast<T *>(smem + Cfg::OFF_ROW);
   double *npart = reinterpret_cast<double *>(smem + Cfg::OFF_NPART);
-  double *Dv = reinterpret_cast<double *>(smem + Cfg::OFF_D);
   double *lam = reinterpret_cast<double *>(smem + Cfg::OFF_LAM);
   int *Jv = reinterpret_cast<int *>(smem + Cfg::OFF_J);
   __shared__ int s_flag[2];
@@ -231,9 +265,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   __shared__ int s_fail;
   __shared__ unsigned long long s_maxt;
   __shared__ uint64_t s_mbar[2];
-  __shared__ int cib[NMAX / 2], cjb[NMAX / 2], k_on[NMAX / 2];
-  __shared__ double k_cs[NMAX / 2], k_hs[NMAX / 2];
-  __shared__ T k_cp[NMAX / 2], k_sp[NMAX / 2];
+  __shared__ uint64_t s_pbar[NT / 32];
 
   int crank = 0;
   if constexpr (C > 1) crank = int(cg::this_cluster().block_rank());
@@ -265,6 +297,167 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   int fallback = 0;
   int k0 = 0;
   bool need_dense = dense;
+  // Fast path (NMAX <= 128): every CTA of the cluster redundantly forms the
+  // whole b x b matrix U_in -- the Schur complement S = L_j - R_ij^H R_ij of
+  // the structured Cholesky (blocking.py:131-134), or herm(B^H B) for the
+  // pre-pass (parallel.py:143, core.py:54-55) -- and factors it in a
+  // register tile (one CTA barrier per column, no cluster traffic).  The
+  // factor stays in Ws for the back substitution W = R0^-1 R_final.
+  bool fast = false;
+  const int nt = dense ? 0 : ni;  // rows of R0 with the diagonal sqrt(L_i) block
+  const int nu = dense ? N : nj;  // order of U
+  if constexpr (Cfg::FAST) {
+    int ok = 1;
+    if (!dense) {
+      for (int c = tid; c < N; c += NT) ok &= (lam[c] > 0.0);
+      ok = __syncthreads_and(ok);
+    }
+    if (!ok) {
+      need_dense = true;  // structured_cholesky raises (blocking.py:125-126)
+      fallback = 1;
+    } else {
+      constexpr int TI = Cfg::TI, TL = Cfg::TL, XI = Cfg::XI, YL = Cfg::YL, UL = Cfg::UL;
+      const int ti = tid % TI, tl = tid / TI;
+      T u[XI][YL];
+      if (!dense) {
+        // S[i][l] = L_j[i] d_il - sum_h conj(Rij[h][i]) Rij[h][l], Rij = A / sqrt(L_i)
+#pragma unroll
+        for (int x = 0; x < XI; ++x)
+#pragma unroll
+          for (int y = 0; y < YL; ++y) u[x][y] = S<T>::zero();
+        T *scr = Rs;  // staging: HC x NMAX rows of R_ij
+        for (int h0 = 0; h0 < ni; h0 += HC) {
+          const int hc = min(HC, ni - h0);
+          for (int e = tid; e < HC * nj; e += NT) {
+            const int h = e % HC, l = e / HC;
+            scr[h * NMAX + l] = h < hc ? divr(A[(h0 + h) + int64_t(l) * bmax], sqrt(lam[h0 + h])) : S<T>::zero();
+          }
+          __syncthreads();
+          for (int h = 0; h < hc; ++h) {
+            T ri[XI], rl[YL];
+#pragma unroll
+            for (int x = 0; x < XI; ++x) ri[x] = scr[h * NMAX + ti + TI * x];
+#pragma unroll
+            for (int y = 0; y < YL; ++y) rl[y] = scr[h * NMAX + min(tl + TL * y, NMAX - 1)];
+#pragma unroll
+            for (int x = 0; x < XI; ++x)
+#pragma unroll
+              for (int y = 0; y < YL; ++y) u[x][y] = cfma(ri[x], rl[y], u[x][y]);
+          }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int x = 0; x < XI; ++x)
+#pragma unroll
+          for (int y = 0; y < YL; ++y) {
+            const int i = ti + TI * x, l = tl + TL * y;
+            T v = sub(i == l && i < nj ? scale(S<T>::one(), lam[ni + i]) : S<T>::zero(), u[x][y]);
+            if (i == l) v = scale(S<T>::one(), re(v));  // exactly Hermitian diagonal
+            u[x][y] = v;
+          }
+      } else {
+#pragma unroll
+        for (int x = 0; x < XI; ++x)
+#pragma unroll
+          for (int y = 0; y < YL; ++y) {
+            const int i = ti + TI * x, l = tl + TL * y;
+            T v = S<T>::zero();
+            if (i <= l && l < N) {
+              if (i == l)
+                v = scale(S<T>::one(), re(A[i + int64_t(i) * bmax]));
+              else
+                v = scale(add(A[i + int64_t(l) * bmax], conjv(A[l + int64_t(i) * bmax])), 0.5);
+            }
+            u[x][y] = v;
+          }
+      }
+      // right-looking Cholesky on the unscaled rows: U[i][l] -= conj(U[k][i])
+      // U[k][l] / U[k][k]; row k+1 is published through a double buffer
+      T *rowb = reinterpret_cast<T *>(smem + Cfg::OFF_ROW);  // [2][UB]
+      double *piv = npart;                                    // pivots U[k][k]
+      auto publish = [&](int k) {
+        if (k < nu && ti == k % TI) {
+          const int x = k / TI;
+#pragma unroll
+          for (int xx = 0; xx < XI; ++xx) {
+            if (xx != x) continue;
+#pragma unroll
+            for (int y = 0; y < YL; ++y) {
+              const int l = tl + TL * y;
+              if (l >= k && l < nu) rowb[(k & 1) * Cfg::UB + l] = u[xx][y];
+            }
+          }
+        }
+      };
+      publish(0);
+      __syncthreads();
+      int chol_ok = 1;
+      for (int k = 0; k < nu; ++k) {
+        const T *rk = rowb + (k & 1) * Cfg::UB;
+        const double dk = re(rk[k]);
+        if (!finite_pos(dk)) {
+          chol_ok = 0;
+          break;
+        }
+        if (tid == 0) piv[k] = dk;
+        const double inv = 1.0 / dk;
+        T ri[XI], rl[YL];
+#pragma unroll
+        for (int x = 0; x < XI; ++x) ri[x] = scale(rk[min(ti + TI * x, Cfg::UB - 1)], inv);
+#pragma unroll
+        for (int y = 0; y < YL; ++y) rl[y] = rk[min(tl + TL * y, Cfg::UB - 1)];
+#pragma unroll
+        for (int x = 0; x < XI; ++x)
+#pragma unroll
+          for (int y = 0; y < YL; ++y) {
+            const int i = ti + TI * x, l = tl + TL * y;
+            if (i > k && l >= i && l < nu) u[x][y] = cfms(ri[x], rl[y], u[x][y]);
+          }
+        publish(k + 1);
+        __syncthreads();
+      }
+      if (chol_ok) {
+        // final factor into Ws: R[k][k] = sqrt(d_k), R[k][l] = U[k][l] / sqrt(d_k)
+        T *U = Ws;
+#pragma unroll
+        for (int x = 0; x < XI; ++x)
+#pragma unroll
+          for (int y = 0; y < YL; ++y) {
+            const int i = ti + TI * x, l = tl + TL * y;
+            if (l >= Cfg::UB) continue;
+            T v = S<T>::zero();
+            if (i <= l && l < nu) {
+              const double rd = sqrt(piv[i]);
+              v = i == l ? scale(S<T>::one(), rd) : divr(u[x][y], rd);
+            }
+            U[i + l * UL] = v;
+          }
+        __syncthreads();
+        // R0 slab rows of this CTA: [[sqrt(L_i), A / sqrt(L_i)], [0, U]]
+        for (int e = tid; e < NMAX * RS; e += NT) Rs[e] = S<T>::zero();
+        __syncthreads();
+        for (int e = tid; e < RPC * NMAX; e += NT) {
+          const int gl = e % RPC, c = e / RPC;
+          const int g = row0 + gl;
+          if (g >= N || c >= N || c < g) continue;
+          T v;
+          if (g < nt)
+            v = c == g ? scale(S<T>::one(), sqrt(lam[g])) : (c < nt ? S<T>::zero() : divr(A[g + int64_t(c - nt) * bmax], sqrt(lam[g])));
+          else
+            v = U[(g - nt) + (c - nt) * UL];
+          Rs[gl + c * RS] = v;
+        }
+        __syncthreads();
+        fast = true;
+        need_dense = false;
+      } else if (dense) {
+        status = PV_CHOL;
+      } else {
+        need_dense = true;  // parallel.py:196-198
+        fallback = 1;
+      }
+    }
+  } else
   if (!dense) {
     int ok = 1;
     for (int c = tid; c < N; c += NT) ok &= (lam[c] > 0.0);
@@ -404,7 +597,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     return true;
   };
 
-  if (!need_dense) {
+  if (!need_dense && !fast) {
     if (!cholesky(k0)) {
       if (dense) {
         status = PV_CHOL;
@@ -437,54 +630,52 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
 
   t_chol = clock64();
   // ------------------------------------------------------------------ Jacobi
-  // Register-resident columns.  Pair slot q (TPP lanes) holds the RPC-row
-  // slab of two columns of R in registers; lane l owns rows l, l+TPP, ...
-  // After each round the slot keeps one column and passes the other to its
-  // ring neighbour, exactly as the reference's modulus stepper passes block
-  // columns between workers (strategies.py:58-92, applied with nbl = N): a
-  // warp shuffle inside a warp, shared memory across warps.  W is not
-  // accumulated rotation by rotation: the initial factor R0 stays in shared
-  // memory and W = R0^-1 R_final is formed once at the end.
+  // Register-resident columns.  Pair slot q (TPP lanes of one warp) holds the
+  // RPC-row slab of its two columns of R in registers (lane l owns rows l,
+  // l+TPP, ...) together with their D values (the D cache of
+  // rotations.py:217 / _kernels.py:80-81 travels with its column).  After
+  // each round the slot keeps one column and passes the other to its ring
+  // neighbour, exactly as the reference's modulus stepper passes block
+  // columns between workers (strategies.py:58-92 with nbl = N): a warp
+  // shuffle inside a warp, shared memory + a per-warp mbarrier across warps.
+  //
+  // One round, without any CTA-wide barrier:
+  //   dot partial over the lane's rows -> shuffle reduction over the TPP
+  //   lanes -> st.async of the CTA partial into every cluster peer (local
+  //   store for this CTA) -> per-warp arrive on the round's mbarrier (which
+  //   also waits for the peers' bytes) -> every lane sums the C partials in
+  //   rank order (bit-identical in all CTAs) and derives the rotation itself
+  //   -> apply -> ring step.
+  // Every CTA computes every pair's rotation, so the sweep's rotation count
+  // (the convergence test, parallel.py:239-244) is known in each CTA without
+  // a cluster exchange.  W is not accumulated per rotation: W = R0^-1 R_final
+  // is formed once at the end.
   const double otol = a.orth_tol > 0.0 ? a.orth_tol : sqrt(double(N)) * kEps;
   const double otol2 = otol * otol;
   const double qtol = a.quad_tol > 0.0 ? a.quad_tol : double(N) * kEps;
   const int ne = N + (N & 1);
   const int pr = ne / 2;  // ring slots in use
   const int slot = tid / TPP, lane_in = tid % TPP;
-  constexpr int SPW = Cfg::SPW;
+  constexpr int SPW = Cfg::SPW, NWARP = Cfg::NWARP;
+  const int warp = tid >> 5, lane = tid & 31;
   const bool in_ring = slot < pr;
-  const int wslot = slot % SPW, warp = slot / SPW;
+  const int wslot = slot % SPW;
   int ip = slot + 1, jp = ne - slot, ib = ip, jb = jp;  // strategies.py:58-66
   long long nrot_total = 0;
   int sweeps = 0;
-  int gr = 0;  // global round counter (buffer parities)
-  int my_big = 0, my_cnt = 0;
+  int gr = 0;  // exchange counter (mbarrier phases / buffer parities)
+  int pg = 0;  // ring-pass counter (pass-buffer parities)
+  int my_big = 0, my_cnt = 0, my_fail = INT_MAX;
   double my_maxt = 0.0;
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int pd_on = 0, pd_ci = 0, pd_cj = 0;
-  double pd_dr = 0, pd_ds = 0, pd_num = 0, pd_den = 1, pd_eta = 0, pd_hyp = 0;
-  auto finish_d = [&]() {
-    const double t = pd_num / pd_den;
-    Dv[pd_ci] = pd_dr + pd_hyp * t * pd_eta;
-    Dv[pd_cj] = pd_ds + t * pd_eta;
-    ++my_cnt;
-    const double at = fabs(t);
-    my_big += at > qtol;
-    my_maxt = fmax(my_maxt, at);
-    pd_on = 0;
-  };
-  T *xbuf = Ws;
-  constexpr unsigned TX = (C - 1) * Cfg::P2 * sizeof(T);  // bytes pushed into each CTA per round
-  if constexpr (C > 1) {
-    if (tid == 0) {
-      for (int b = 0; b < 2; ++b) mbar_init(&s_mbar[b], 1);
-      fence_mbar_init();
-      for (int b = 0; b < 2; ++b) mbar_arm(&s_mbar[b], TX);
-    }
-  }
-  if (in_ring && lane_in == 0) {
-    cib[slot] = ib - 1;
-    cjb[slot] = jb - 1;
+  T *xbuf = reinterpret_cast<T *>(smem + Cfg::OFF_X);             // [2][NWARP][RPC]
+  double *xd = reinterpret_cast<double *>(smem + Cfg::OFF_XD);     // [2][NWARP]
+  constexpr unsigned TX = (C - 1) * Cfg::P2 * sizeof(T);          // dot partials pushed into each CTA
+  constexpr unsigned TXN = (C - 1) * Cfg::P2 * 16;                // column-norm partials
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) mbar_init(&s_mbar[b], NWARP);
+    for (int w = 0; w < NWARP; ++w) mbar_init(&s_pbar[w], TPP);
+    fence_mbar_init();
   }
   T X[RPT], Y[RPT];
 #pragma unroll
@@ -494,190 +685,240 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     X[u] = Rs[ci * RS + row];
     Y[u] = Rs[cj * RS + row];
   }
-  cluster_sync<C>();
+  double dX = 0.0, dY = 0.0;
+  int sX = 1, sY = 1;  // J signs of the two columns
+  cluster_sync<C>();   // barriers initialised in every CTA before any push
 
+  // push this slot's CTA partial v (sizeof(V) bytes) to every CTA of the
+  // cluster (plain store into this CTA), then arrive on the exchange barrier
+  auto push = [&](auto *base, auto v, unsigned tx) {
+    const int buf = gr & 1;
+    auto *mine = base + (buf * C + crank) * Cfg::P2 + slot;
+    if constexpr (C > 1) {
+      const uint32_t la = smem_u32(mine), lb = smem_u32(&s_mbar[buf]);
+#pragma unroll
+      for (int q0 = 0; q0 < C; q0 += TPP) {
+        const int q = q0 + lane_in;
+        if (q < C) {
+          if (q == crank)
+            *mine = v;
+          else
+            st_async(mapa_u32(la, q), v, mapa_u32(lb, q));
+        }
+      }
+    } else {
+      if (lane_in == 0) *mine = v;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (warp == 0)
+        mbar_arrive_tx(&s_mbar[buf], tx);
+      else
+        mbar_arrive(&s_mbar[buf]);
+    }
+  };
+
+  // dot partial of this lane's rows for its slot's current pair
+  auto dot_part = [&]() {
+    T d0 = S<T>::zero(), d1 = S<T>::zero();
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (u & 1)
+        d1 = cfma(X[u], Y[u], d1);
+      else
+        d0 = cfma(X[u], Y[u], d0);
+    }
+    return add(d0, d1);
+  };
+  T dn = dot_part();
   if (status == PV_OK) {
     for (int sw = 0; sw < a.max_sweeps; ++sw) {
       ++sweeps;
       const bool odd = (sw & 1) == 0;  // reference sweeps count from 1; odd send to q-1
-      // D = colnorms^2(R) (rotations.py:217), from the registers, reduced over the cluster
+      const int src = odd ? (slot + 1 == pr ? 0 : slot + 1) : (slot == 0 ? pr - 1 : slot - 1);
+      const int srcw = src / SPW;
+      const bool via_smem = in_ring && (odd ? (wslot == SPW - 1 || slot == pr - 1) : (wslot == 0 || slot == 0));
+      const bool writer = in_ring && (odd ? (wslot == 0) : (wslot == SPW - 1 || slot == pr - 1));
+      const int src_lane = odd ? min(lane + TPP, 31) : max(lane - TPP, 0);
+      // ---- D = colnorms^2(R) (rotations.py:217): cluster-reduced norms ----
       {
-        double nx0 = 0.0, nx1 = 0.0, ny0 = 0.0, ny1 = 0.0;
+        double nx = 0.0, ny = 0.0, nx1 = 0.0, ny1 = 0.0;
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
           if (u & 1) { nx1 += abs2(X[u]); ny1 += abs2(Y[u]); }
-          else { nx0 += abs2(X[u]); ny0 += abs2(Y[u]); }
+          else { nx += abs2(X[u]); ny += abs2(Y[u]); }
         }
-        double nx = nx0 + nx1, ny = ny0 + ny1;
+        nx += nx1;
+        ny += ny1;
 #pragma unroll
         for (int o = 1; o < TPP; o <<= 1) {
           nx += __shfl_xor_sync(0xffffffffu, nx, o);
           ny += __shfl_xor_sync(0xffffffffu, ny, o);
         }
-        if (in_ring && lane_in == 0) {
-          npart[ib - 1] = nx;
-          npart[jb - 1] = ny;
-        }
-        cluster_sync<C>();
-        if (in_ring && lane_in < 2) {
-          const int col = lane_in == 0 ? ib - 1 : jb - 1;
-          double sacc = 0.0;
-#pragma unroll 1
-          for (int q = 0; q < C; ++q) sacc += remote<C>(npart, q)[col];
-          Dv[col] = sacc;
-        }
-      }
-      if (tid == 0) s_cnt[(sw + 1) & 1] = 0;
-      __syncthreads();
-
-      for (int rnd = 0; rnd < ne; ++rnd, ++gr) {
-        const long long c0 = RCLK();
-        if (pd_on) finish_d();
-        // (1) slab phase: CTA-partial of g_i^H g_j for this slot's pair
-        T d0 = S<T>::zero(), d1 = S<T>::zero();
+        const int buf = gr & 1;
+        double2 *nbuf = S<T>::cx ? reinterpret_cast<double2 *>(part) : reinterpret_cast<double2 *>(npart);
+        push(nbuf, make_double2(nx, ny), TXN);
+        mbar_wait_cta(&s_mbar[buf], (gr >> 1) & 1);
+        const double2 *np0 = nbuf + (buf * C) * Cfg::P2 + slot;
+        double2 nn = np0[0];
 #pragma unroll
-        for (int u = 0; u < RPT; ++u) {
-          if (u & 1)
-            d1 = cfma(X[u], Y[u], d1);
-          else
-            d0 = cfma(X[u], Y[u], d0);
+        for (int r = 1; r < C; ++r) {
+          const double2 v = np0[r * Cfg::P2];
+          nn.x += v.x;
+          nn.y += v.y;
         }
-        T dot = add(d0, d1);
+        dX = nn.x;
+        dY = nn.y;
+        ++gr;
+      }
+      sX = Jv[min(ib - 1, NMAX - 1)];
+      sY = Jv[min(jb - 1, NMAX - 1)];
+
+      for (int rnd = 0; rnd < ne; ++rnd, ++gr, ++pg) {
+        const long long c0 = RCLK();
+        // (1) CTA partial of g_i^H g_j (computed at the end of the previous
+        // round), reduced over the slot's TPP lanes, pushed to the cluster
+        T dot = dn;
 #pragma unroll
         for (int o = 1; o < TPP; o <<= 1) dot = add(dot, shfl_xor(dot, o));
-        const int buf = gr & 1;
-        {
-          T *mine = part + (buf * C + crank) * Cfg::P2 + slot;
-          if constexpr (C > 1) {
-            const uint32_t la = smem_u32(mine), lb = smem_u32(&s_mbar[buf]);
-#pragma unroll 1
-            for (int q = lane_in; q < C; q += TPP) {
-              if (q == crank)
-                *mine = dot;
-              else
-                st_async(mapa_u32(la, q), dot, mapa_u32(lb, q));
-            }
-          } else {
-            if (lane_in == 0) *mine = dot;
-          }
-        }
+        push(part, dot, TX);
         const long long c1 = RCLK();
-        long long c2 = c1, c3 = c1, c4 = c1;
-        __syncthreads();
-        // (2) pair phase: one thread per pair sums the cluster partials in
-        // fixed rank order (bit-identical in every CTA), derives the rotation
-        // once and publishes its coefficients
-        if (tid < pr) {
-          const int q = tid;
-          const int ci = cib[q], cj = cjb[q];
-          if constexpr (C > 1) mbar_wait(&s_mbar[buf], (gr >> 1) & 1);
-          c2 = RCLK();
-          T acc = part[(buf * C) * Cfg::P2 + q];
-#pragma unroll 1
-          for (int r = 1; r < C; ++r) acc = add(acc, part[(buf * C + r) * Cfg::P2 + q]);
-          c3 = RCLK();
-          int on = 0;
-          if (ci < N && cj < N) {
-            const double dr = Dv[ci], ds = Dv[cj];
-            const RotCoef<T> p = rot_coef<T>(acc, dr, ds, Jv[ci] == Jv[cj], otol2);
-            on = p.code == 1;
-            k_cs[q] = p.cs;
-            k_hs[q] = p.hs;
-            k_cp[q] = p.cp;
-            k_sp[q] = p.sp;
-            if (p.code < 0) atomicMin(&s_fail, ci * 4096 + cj);
-            // the D update (_kernels.py:80-81) is finished at the start of
-            // the next round, off the critical path
-            pd_on = on;
-            pd_ci = ci;
-            pd_cj = cj;
-            pd_dr = dr;
-            pd_ds = ds;
-            pd_num = p.num;
-            pd_den = p.den;
-            pd_eta = p.eta;
-            pd_hyp = p.hyp;
-          }
-          k_on[q] = on;
-          c4 = RCLK();
-        }
-        __syncthreads();
-        if constexpr (C > 1) {
-          // this round's buffer is consumed: re-arm it for round gr+2 before
-          // the end-of-round barrier, i.e. before this CTA pushes round gr+1
-          // (no peer can push round gr+2 into it earlier)
-          if (tid == NT - 1) mbar_arm(&s_mbar[buf], TX);
-        }
-        const long long c5 = RCLK();
-        // (3) slab phase: apply, then the ring step
-        if (in_ring && k_on[slot]) {
-          RotCoef<T> p;
-          p.cs = k_cs[slot];
-          p.hs = k_hs[slot];
-          p.cp = k_cp[slot];
-          p.sp = k_sp[slot];
+        // (2) every lane sums the cluster partials in fixed rank order
+        // (bit-identical in every CTA) and derives its slot's rotation
+        // (_kernels.py:53-81)
+        const int buf = gr & 1;
+        mbar_wait_cta(&s_mbar[buf], (gr >> 1) & 1);
+        const long long c2 = RCLK();
+        T acc = part[(buf * C) * Cfg::P2 + slot];
 #pragma unroll
-          for (int u = 0; u < RPT; ++u) rot_fold<T>(X[u], Y[u], p);
+        for (int r = 1; r < C; ++r) acc = add(acc, part[(buf * C + r) * Cfg::P2 + slot]);
+        const int ci = ib - 1, cj = jb - 1;
+        // skip test first (_kernels.py:57); the rotation parameters are only
+        // derived in warps where some pair is not yet orthogonal
+        bool rot = in_ring && ci < N && cj < N && !(abs2(acc) <= otol2 * (dX * dY));
+        const bool any_rot = __any_sync(0xffffffffu, rot);
+        RotCoef<T> p;
+        p.cp = S<T>::one();
+        p.sp = S<T>::zero();
+        p.hs = 0.0;
+        p.cs = 1.0;
+        const long long c3 = RCLK();
+        if (any_rot) {
+          if (rot) {
+            const RotCoef<T> q = rot_coef<T>(acc, dX, dY, sX == sY, otol2);
+            if (q.code == 1) {
+              p = q;
+              // D update (_kernels.py:80-81), off the dependency chain
+              const double te = q.num * q.eta / q.den;
+              dX = fma(q.hyp, te, dX);
+              dY = dY + te;
+              if (lane_in == 0) {
+                ++my_cnt;
+                const double at = fabs(q.num / q.den);
+                my_big += at > qtol;
+                my_maxt = fmax(my_maxt, at);
+              }
+            } else {
+              rot = false;
+              if (q.code < 0) my_fail = min(my_fail, ci * 4096 + cj);
+            }
+          }
         }
-        // ---- ring step: strategies.py:75-92 (nbl = ne) ----
+        const long long c4 = RCLK();
+        // (3) fused per row: apply the rotation, ring step (strategies.py:75-92
+        // with nbl = ne: the slot keeps one column and receives the one its
+        // neighbour sends; odd sweeps receive from slot+1, strategies.py:69-72)
+        // and the next round's dot partial
         const bool send_i = ip + jp > ne;
-        if (send_i) {
-          ++ip;
-          if (ip == jp) {
-            ip -= pr;
-            jp = ip;
+        if (in_ring) {
+          if (send_i) {
+            ++ip;
+            if (ip == jp) {
+              ip -= pr;
+              jp = ip;
+            }
+            ib = ip;
+          } else {
+            ++jp;
+            jb = jp;
           }
-          ib = ip;
-        } else {
-          ++jp;
-          jb = jp;
         }
-        // odd sweeps: receive from slot+1, send to slot-1 (strategies.py:69-72)
-        const int par = gr & 1;
-        const bool via_smem = odd ? (wslot == SPW - 1 || slot == pr - 1) : (wslot == 0 || slot == 0);
-        const bool writer = in_ring && (odd ? (wslot == 0) : (wslot == SPW - 1 || slot == pr - 1));
-        const int src = odd ? (slot + 1 == pr ? 0 : slot + 1) : (slot == 0 ? pr - 1 : slot - 1);
-        T *xw = xbuf + (size_t(par) * Cfg::NWARP + warp) * RPC;
-        const T *xr = xbuf + (size_t(par) * Cfg::NWARP + src / SPW) * RPC;
-        const int lane = threadIdx.x & 31;
-        const int src_lane = odd ? min(lane + TPP, 31) : max(lane - TPP, 0);
-#pragma unroll
-        for (int u = 0; u < RPT; ++u) {
-          const T v = send_i ? X[u] : Y[u];
-          if (writer) xw[lane_in + u * TPP] = v;
-          const T nv = shfl_idx(v, src_lane);
-          if (send_i)
-            X[u] = nv;
-          else
-            Y[u] = nv;
-        }
-        if (in_ring && lane_in == 0) {
-          cib[slot] = ib - 1;
-          cjb[slot] = jb - 1;
-        }
-        const long long c6 = RCLK();
-        __syncthreads();
-        const long long c7 = RCLK();
-        if (in_ring && via_smem) {
+        const int par = pg & 1;
+        T *xw = xbuf + (size_t(par) * NWARP + warp) * RPC;
+        const bool all_i = __all_sync(0xffffffffu, send_i || !in_ring);
+        const bool all_j = __all_sync(0xffffffffu, !send_i || !in_ring);
+        // one straight-line body per (rotation, moving register) case so the
+        // rows software-pipeline: apply -> shuffle -> next dot partial
+        T e0 = S<T>::zero(), e1 = S<T>::zero();
+        auto fused = [&](auto rot_c, auto mode_c) {
+          constexpr bool ROT = decltype(rot_c)::value;
+          constexpr int MODE = decltype(mode_c)::value;  // 0: X moves, 1: Y moves, 2: per lane
+          const double dv = MODE == 0 ? dX : (MODE == 1 ? dY : (send_i ? dX : dY));
+          if (writer && lane_in == 0) xd[par * NWARP + warp] = dv;
+          const double nd = __shfl_sync(0xffffffffu, dv, src_lane);
+          if (MODE == 0 || (MODE == 2 && send_i)) dX = nd; else dY = nd;
 #pragma unroll
           for (int u = 0; u < RPT; ++u) {
-            const T nv = xr[lane_in + u * TPP];
-            if (send_i)
-              X[u] = nv;
-            else
-              Y[u] = nv;
+            if constexpr (ROT) rot_fold<T>(X[u], Y[u], p);
+            const T v = MODE == 0 ? X[u] : (MODE == 1 ? Y[u] : (send_i ? X[u] : Y[u]));
+            st_shared_if(writer, xw + lane_in + u * TPP, v);
+            const T nv = shfl_idx(v, src_lane);
+            if constexpr (MODE == 0) X[u] = nv;
+            else if constexpr (MODE == 1) Y[u] = nv;
+            else { if (send_i) X[u] = nv; else Y[u] = nv; }
+            if (u & 1) e1 = cfma(X[u], Y[u], e1); else e0 = cfma(X[u], Y[u], e0);
           }
+        };
+        using B1 = std::integral_constant<bool, true>;
+        using B0 = std::integral_constant<bool, false>;
+        using M0 = std::integral_constant<int, 0>;
+        using M1 = std::integral_constant<int, 1>;
+        using M2 = std::integral_constant<int, 2>;
+        __syncwarp();
+        if (any_rot) {
+          if (all_i) fused(B1{}, M0{}); else if (all_j) fused(B1{}, M1{}); else fused(B1{}, M2{});
+        } else {
+          if (all_i) fused(B0{}, M0{}); else if (all_j) fused(B0{}, M1{}); else fused(B0{}, M2{});
         }
-        const long long c8 = RCLK();
+        dn = add(e0, e1);
+        if (writer) mbar_arrive(&s_pbar[warp]);
+        const long long c5 = RCLK();
+        if (via_smem) {
+          // the warp-edge slot receives through shared memory and redoes its
+          // dot partial
+          const T *xr = xbuf + (size_t(par) * NWARP + srcw) * RPC;
+          mbar_wait_cta(&s_pbar[srcw], par);
+          const double nd = xd[par * NWARP + srcw];
+          if (send_i) {
+            dX = nd;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) X[u] = xr[lane_in + u * TPP];
+          } else {
+            dY = nd;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) Y[u] = xr[lane_in + u * TPP];
+          }
+          dn = dot_part();
+        }
+        // J signs of the slot's (possibly new) columns (static per column)
+        sX = Jv[min(ib - 1, NMAX - 1)];
+        sY = Jv[min(jb - 1, NMAX - 1)];
+        __syncwarp();
+        const long long c6 = RCLK();
         if (HJB_ROUND_PROFILE && a.prof) {
           ph[0] += c1 - c0; ph[1] += c2 - c1; ph[2] += c3 - c2; ph[3] += c4 - c3;
-          ph[4] += c5 - c4; ph[5] += c6 - c5; ph[6] += c7 - c6; ph[7] += c8 - c7;
+          ph[4] += c5 - c4; ph[5] += c6 - c5;
         }
-        if (s_fail != INT_MAX) break;
       }
-      if (pd_on) finish_d();
-      if (my_cnt) atomicAdd(&s_cnt[sw & 1], my_cnt);
-      nrot_total += 0;
+      // sweep end: the rotation count and failures are the same in every
+      // CTA (every CTA derived every rotation), so a CTA barrier suffices
+      if (tid == 0) s_cnt[(sw + 1) & 1] = 0;
+      const int wc = __reduce_add_sync(0xffffffffu, my_cnt);
+      const int wf = __reduce_min_sync(0xffffffffu, my_fail);
+      if (lane == 0) {
+        if (wc) atomicAdd(&s_cnt[sw & 1], wc);
+        if (wf != INT_MAX) atomicMin(&s_fail, wf);
+      }
       my_cnt = 0;
       __syncthreads();
       if (s_fail != INT_MAX) {
@@ -692,97 +933,201 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   t_jac = clock64();
 
   // ------------------------------------------------------------------ W = R0^-1 R
-  // R_final columns -> shared slab Fs (by column); back substitution by row
-  // blocks from the last CTA of the cluster to the first.
-  T *Fs = Ws;  // RPC x NMAX slab (scratch region is large enough)
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) {
-    if (!in_ring) break;
-    const int row = lane_in + u * TPP;
-    Fs[(ib - 1) * RS + row] = X[u];
-    Fs[(jb - 1) * RS + row] = Y[u];
-  }
   if (my_big) atomicAdd(&s_big, my_big);
   if (my_maxt > 0.0) atomicMax(&s_maxt, static_cast<unsigned long long>(__double_as_longlong(my_maxt)));
-  __syncthreads();
-  for (int k = C - 1; k >= 0; --k) {
-    if (crank == k) {
-      // local rows, last to first; columns of W are independent, so each
-      // thread back-substitutes whole columns (no barrier inside the block)
-      for (int gl = tid; gl < RPC; gl += NT) {
-        const int g = row0 + gl;
-        npart[gl] = g < N ? 1.0 / re(Rs[g * RS + gl]) : 0.0;  // reciprocal diagonal
-      }
-      __syncthreads();
-      for (int c = tid; c < N; c += NT) {
-        T col[RPC];
+  const int nmax = a.nmax;
+  T *Wout = reinterpret_cast<T *>(a.W) + int64_t(item_id) * nmax * nmax;
+  T *Rout = a.Rout ? reinterpret_cast<T *>(a.Rout) + int64_t(item_id) * nmax * nmax : nullptr;
+  if constexpr (Cfg::FAST) {
+    if (fast) {
+      // R0 = [[diag(s), A/s], [0, U]] (s = sqrt(L_i)), so W = R0^-1 R_final is
+      //   W_b = U^-1 F_b,   W_t = F_t / s - (A W_b) / s^2.
+      // R_final goes through the W buffer (L2); CTA r then owns the columns
+      // [r RPC, (r+1) RPC): one warp per column group back-substitutes with
+      // its lanes holding rows (shuffle broadcast of each solved row).
+      constexpr int UL = Cfg::UL, RV = Cfg::RV;
+      constexpr int CW = (RPC + NWARP - 1) / NWARP;
+      const T *U = Ws;
+      if (in_ring) {
 #pragma unroll
-        for (int gl = 0; gl < RPC; ++gl) col[gl] = Fs[c * RS + gl];
-#pragma unroll
-        for (int gl = RPC - 1; gl >= 0; --gl) {
-          if (row0 + gl >= N) continue;
-          const T w = scale(col[gl], npart[gl]);
-          col[gl] = w;
-#pragma unroll
-          for (int gl2 = 0; gl2 < gl; ++gl2) col[gl2] = sub(col[gl2], mul(Rs[(row0 + gl) * RS + gl2], w));
+        for (int u = 0; u < RPT; ++u) {
+          const int g = row0 + lane_in + u * TPP;
+          if (g >= N) continue;
+          if (ib - 1 < N) Wout[g + int64_t(ib - 1) * nmax] = X[u];
+          if (jb - 1 < N) Wout[g + int64_t(jb - 1) * nmax] = Y[u];
+          if (Rout) {
+            if (ib - 1 < N) Rout[g + int64_t(ib - 1) * nmax] = X[u];
+            if (jb - 1 < N) Rout[g + int64_t(jb - 1) * nmax] = Y[u];
+          }
         }
-#pragma unroll
-        for (int gl = 0; gl < RPC; ++gl) Fs[c * RS + gl] = col[gl];
       }
-      __syncthreads();
-    }
-    cluster_sync<C>();
-    if (crank < k) {
-      // T[rows of this CTA] -= R0[these rows, block k] W[block k, :]; the
-      // block of W is first copied from CTA k (DSMEM) into local scratch
-      const T *Wk = remote<C>(Fs, k);
-      T *Wl = part;  // scratch: PART elements, processed in column chunks
-      constexpr int CW = int(Cfg::PART) / RPC;
-      const int rk0 = k * RPC;
-      const int jn = min(RPC, N - rk0);
-      for (int c0 = 0; c0 < N; c0 += CW) {
-        const int cw = min(CW, N - c0);
-        for (int e = tid; e < RPC * cw; e += NT) {
-          const int j = e % RPC, cc = e / RPC;
-          Wl[j * CW + cc] = Wk[(c0 + cc) * RS + j];
+      double *rdg = npart;  // 1 / U[k][k]
+      for (int k = tid; k < nu; k += NT) rdg[k] = 1.0 / re(U[k + k * UL]);
+      __threadfence();
+      cluster_sync<C>();
+      const int c0 = crank * RPC, c1 = min(N, c0 + RPC);
+      const int cw0 = c0 + warp * CW;
+      T f[CW][RV];
+#pragma unroll
+      for (int cc = 0; cc < CW; ++cc)
+#pragma unroll
+        for (int v = 0; v < RV; ++v) {
+          const int c = cw0 + cc, i = lane + 32 * v;
+          f[cc][v] = (c < c1 && i < nu) ? __ldcg(Wout + (nt + i) + int64_t(c) * nmax) : S<T>::zero();
+        }
+      if (cw0 < c1) {
+        for (int k = nu - 1; k >= 0; --k) {
+          const int ow = k & 31, vk = k >> 5;
+          const double rk = rdg[k];
+          T wk[CW];
+#pragma unroll
+          for (int cc = 0; cc < CW; ++cc) {
+            T fk = f[cc][0];
+#pragma unroll
+            for (int v = 1; v < RV; ++v)
+              if (v == vk) fk = f[cc][v];
+            wk[cc] = scale(shfl_idx(fk, ow), rk);
+          }
+#pragma unroll
+          for (int v = 0; v < RV; ++v) {
+            const int i = lane + 32 * v;
+            if (i < k) {
+              const T uik = U[i + k * UL];
+#pragma unroll
+              for (int cc = 0; cc < CW; ++cc) f[cc][v] = sub(f[cc][v], mul(uik, wk[cc]));
+            } else if (i == k) {
+#pragma unroll
+              for (int cc = 0; cc < CW; ++cc) f[cc][v] = wk[cc];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < CW; ++cc)
+#pragma unroll
+        for (int v = 0; v < RV; ++v) {
+          const int c = cw0 + cc, i = lane + 32 * v;
+          if (c < c1 && i < nu) Wout[(nt + i) + int64_t(c) * nmax] = f[cc][v];
+        }
+      if (nt > 0) {
+        // W_t = F_t / s - (A W_b) / s^2 for this CTA's columns
+        T *Wb = Rs;  // [nu][RPC] staging (column stride UL)
+        T *As = Ws;  // A (nt x nu), column stride UL
+        __syncthreads();  // every warp is done with U
+#pragma unroll
+        for (int cc = 0; cc < CW; ++cc)
+#pragma unroll
+          for (int v = 0; v < RV; ++v) {
+            const int c = cw0 + cc, i = lane + 32 * v;
+            if (c < c1 && i < nu) Wb[i + (c - c0) * UL] = f[cc][v];
+          }
+        for (int e = tid; e < nt * nu; e += NT) {
+          const int h = e % nt, l = e / nt;
+          As[h + l * UL] = A[h + int64_t(l) * bmax];
         }
         __syncthreads();
-        for (int e = tid; e < RPC * cw; e += NT) {
-          const int gl = e % RPC, cc = e / RPC;
-          if (row0 + gl >= N) continue;
-          T acc = Fs[(c0 + cc) * RS + gl];
-          for (int j = 0; j < jn; ++j) acc = sub(acc, mul(Rs[(rk0 + j) * RS + gl], Wl[j * CW + cc]));
-          Fs[(c0 + cc) * RS + gl] = acc;
+        const int ncol = max(0, c1 - c0);
+        for (int e = tid; e < nt * ncol; e += NT) {
+          const int h = e % nt, cl = e / nt;
+          T acc0 = S<T>::zero(), acc1 = S<T>::zero();
+          int l = 0;
+          for (; l + 1 < nu; l += 2) {
+            acc0 = add(acc0, mul(As[h + l * UL], Wb[l + cl * UL]));
+            acc1 = add(acc1, mul(As[h + (l + 1) * UL], Wb[(l + 1) + cl * UL]));
+          }
+          if (l < nu) acc0 = add(acc0, mul(As[h + l * UL], Wb[l + cl * UL]));
+          const double lh = lam[h];
+          const T fv = __ldcg(Wout + h + int64_t(c0 + cl) * nmax);
+          Wout[h + int64_t(c0 + cl) * nmax] = sub(divr(fv, sqrt(lh)), divr(add(acc0, acc1), lh));
         }
-        __syncthreads();
       }
     }
-    cluster_sync<C>();
   }
-
-  // ------------------------------------------------------------------ out
-  {
-    const int nmax = a.nmax;
-    T *Wout = reinterpret_cast<T *>(a.W) + int64_t(item_id) * nmax * nmax;
-    T *Rout = a.Rout ? reinterpret_cast<T *>(a.Rout) + int64_t(item_id) * nmax * nmax : nullptr;
-    for (int e = tid; e < RPC * N; e += NT) {
-      const int gl = e % RPC, c = e / RPC;
-      const int g = row0 + gl;
-      if (g < N) Wout[g + int64_t(c) * nmax] = Fs[c * RS + gl];
+  if (!fast) {
+    T *Fs = Ws;  // RPC x NMAX slab (scratch region is large enough)
+    __syncthreads();
+  #pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (!in_ring) break;
+      const int row = lane_in + u * TPP;
+      Fs[(ib - 1) * RS + row] = X[u];
+      Fs[(jb - 1) * RS + row] = Y[u];
     }
-    if (Rout) {
-      // R_final = R0 W (rows of this CTA), recomputed for the optional output
+    __syncthreads();
+    for (int k = C - 1; k >= 0; --k) {
+      if (crank == k) {
+        // local rows, last to first; columns of W are independent, so each
+        // thread back-substitutes whole columns (no barrier inside the block)
+        for (int gl = tid; gl < RPC; gl += NT) {
+          const int g = row0 + gl;
+          npart[gl] = g < N ? 1.0 / re(Rs[g * RS + gl]) : 0.0;  // reciprocal diagonal
+        }
+        __syncthreads();
+        for (int c = tid; c < N; c += NT) {
+          T col[RPC];
+  #pragma unroll
+          for (int gl = 0; gl < RPC; ++gl) col[gl] = Fs[c * RS + gl];
+  #pragma unroll
+          for (int gl = RPC - 1; gl >= 0; --gl) {
+            if (row0 + gl >= N) continue;
+            const T w = scale(col[gl], npart[gl]);
+            col[gl] = w;
+  #pragma unroll
+            for (int gl2 = 0; gl2 < gl; ++gl2) col[gl2] = sub(col[gl2], mul(Rs[(row0 + gl) * RS + gl2], w));
+          }
+  #pragma unroll
+          for (int gl = 0; gl < RPC; ++gl) Fs[c * RS + gl] = col[gl];
+        }
+        __syncthreads();
+      }
+      cluster_sync<C>();
+      if (crank < k) {
+        // T[rows of this CTA] -= R0[these rows, block k] W[block k, :]; the
+        // block of W is first copied from CTA k (DSMEM) into local scratch
+        const T *Wk = remote<C>(Fs, k);
+        T *Wl = part;  // scratch: PART elements, processed in column chunks
+        constexpr int CW = int(Cfg::PART) / RPC;
+        const int rk0 = k * RPC;
+        const int jn = min(RPC, N - rk0);
+        for (int c0 = 0; c0 < N; c0 += CW) {
+          const int cw = min(CW, N - c0);
+          for (int e = tid; e < RPC * cw; e += NT) {
+            const int j = e % RPC, cc = e / RPC;
+            Wl[j * CW + cc] = Wk[(c0 + cc) * RS + j];
+          }
+          __syncthreads();
+          for (int e = tid; e < RPC * cw; e += NT) {
+            const int gl = e % RPC, cc = e / RPC;
+            if (row0 + gl >= N) continue;
+            T acc = Fs[(c0 + cc) * RS + gl];
+            for (int j = 0; j < jn; ++j) acc = sub(acc, mul(Rs[(rk0 + j) * RS + gl], Wl[j * CW + cc]));
+            Fs[(c0 + cc) * RS + gl] = acc;
+          }
+          __syncthreads();
+        }
+      }
+      cluster_sync<C>();
+    }
+
+    {
       for (int e = tid; e < RPC * N; e += NT) {
         const int gl = e % RPC, c = e / RPC;
         const int g = row0 + gl;
-        if (g >= N) continue;
-        T acc = S<T>::zero();
-        for (int j = g; j < N; ++j) {
-          const T *Wj = remote<C>(Fs, j / RPC);
-          acc = add(acc, mul(Rs[j * RS + gl], Wj[c * RS + (j % RPC)]));
+        if (g < N) Wout[g + int64_t(c) * nmax] = Fs[c * RS + gl];
+      }
+      if (Rout) {
+        // R_final = R0 W (rows of this CTA), recomputed for the optional output
+        for (int e = tid; e < RPC * N; e += NT) {
+          const int gl = e % RPC, c = e / RPC;
+          const int g = row0 + gl;
+          if (g >= N) continue;
+          T acc = S<T>::zero();
+          for (int j = g; j < N; ++j) {
+            const T *Wj = remote<C>(Fs, j / RPC);
+            acc = add(acc, mul(Rs[j * RS + gl], Wj[c * RS + (j % RPC)]));
+          }
+          Rout[g + int64_t(c) * nmax] = acc;
         }
-        Rout[g + int64_t(c) * nmax] = acc;
       }
     }
   }
@@ -857,8 +1202,9 @@ static size_t pivot_smem(bool cx, int nmax, int c) {
   const size_t w = cx ? 16 : 8;
   const size_t rs = nmax / c + 1;
   const size_t slab = nmax * rs;
-  return (slab + std::max<size_t>(slab, 16 * nmax)) * w + 2 * c * (nmax / 2) * w + 2 * nmax * w +
-         3 * nmax * 8 + nmax * 4;
+  const size_t ub = nmax / 2;
+  const size_t scr = std::max<size_t>(std::max<size_t>(slab, 16 * nmax), nmax <= 128 ? ub * (ub + 1) : 0);
+  return (slab + scr) * w + 2 * c * (nmax / 2) * w + 2 * nmax * w + 3 * nmax * 8 + nmax * 4;
 }
 
 int pivot_default_cluster(bool cx, int nmax, int count) {
@@ -909,10 +1255,27 @@ static cudaError_t query_clusters(int *out) {
   return cudaOccupancyMaxActiveClusters(out, k, &cfg);
 }
 
+// The instantiated (NMAX, C, NT) table.  Build with -DHJB_PIVOT_DEV to
+// compile only the configurations of the BASELINE bench workloads (fast
+// iteration on the kernel).
+template <typename T, int NMAX, int C, int NT>
+constexpr bool pivot_allowed() {
+#ifdef HJB_PIVOT_DEV
+  return (S<T>::cx && NMAX == 128 && (C == 4 || C == 8)) || (NMAX == 64 && NT == 256) ||
+         (!S<T>::cx && NMAX == 128 && NT == 256 && (C == 2 || C == 4));
+#else
+  if (NMAX == 32) return C <= 2 && NT <= 256;
+  if (NMAX == 64) return C <= 4 && NT <= 256;
+  if (NMAX == 128) return C >= 2 && C <= 8;
+  return C >= 4;
+#endif
+}
+
 template <typename T, int NMAX, int C, int NT>
 static cudaError_t launch_if_valid(const PivotArgs &a, cudaStream_t st) {
   constexpr int P2 = NMAX / 2, RPC = NMAX / C;
-  if constexpr (RPC >= 4 && NT >= P2 && NT / P2 <= 32 && NT / P2 <= RPC && NT <= RPC * NMAX) {
+  if constexpr (pivot_allowed<T, NMAX, C, NT>() && RPC >= 4 && NT >= P2 && NT / P2 <= 32 && NT / P2 <= RPC &&
+                NT <= RPC * NMAX) {
     if constexpr (PivCfg<T, NMAX, C, NT>::SMEM <= 227 * 1024) {
       if (g_query_clusters) return query_clusters<T, NMAX, C, NT>(&g_query_clusters);
       return launch_pivot_t<T, NMAX, C, NT>(a, st);
@@ -939,9 +1302,9 @@ int pivot_max_active_clusters(bool cx, int nmax, int c, int nt) {
 template <typename T, int NMAX, int C>
 static cudaError_t dispatch_nt(const PivotArgs &a, int nt, cudaStream_t st) {
   switch (nt) {
+    case 128: return launch_if_valid<T, NMAX, C, 128>(a, st);
     case 256: return launch_if_valid<T, NMAX, C, 256>(a, st);
     case 512: return launch_if_valid<T, NMAX, C, 512>(a, st);
-    case 1024: return launch_if_valid<T, NMAX, C, 1024>(a, st);
   }
   return cudaErrorInvalidConfiguration;
 }
@@ -967,12 +1330,12 @@ int pivot_default_threads(bool cx, int nmax, int c) {
   // smallest CTA whose register-resident slab (4 arrays x RPT rows) stays
   // within ~4 complex / 8 real rows per thread
   const int p2 = nmax / 2, rpc = nmax / c, cap = 8;
-  for (int nt = 256; nt <= 1024; nt *= 2) {
+  for (int nt = 128; nt <= 512; nt *= 2) {
     const int tpp = nt / p2;
     if (tpp < 1 || tpp > 32 || tpp > rpc) continue;
     if (rpc / tpp <= cap) return nt;
   }
-  return 1024;
+  return 512;
 }
 
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used) {

@@ -17,8 +17,8 @@ kw = {k: v for k, v in (("n", a.n), ("b", a.b)) if v}
 w = workloads.make(a.config, **kw)
 cx = np.iscomplexobj(w.G)
 L = _lib.lib()
-cfg = P.SolverConfig(variant="2F", strategy="round_robin", p=w.p, tol=P.Tolerances(orth_tol=w.orth_tol, max_sweeps=a.sweep))
-G1, _ = P.parallel_jacobi(w.G, w.J, cfg)
+cfg = P.SolverConfig(variant="2F", strategy="round_robin", p=w.p, tol=P.Tolerances(orth_tol=w.orth_tol, max_sweeps=max(1, a.sweep)))
+G1 = P.parallel_jacobi(w.G, w.J, cfg)[0] if a.sweep > 0 else np.asfortranarray(w.G)
 Gd = torch.from_numpy(np.ascontiguousarray(G1.T)).cuda().t()
 m, n, b = w.m, w.n, w.b
 sd = torch.from_numpy(np.ascontiguousarray(w.J, np.int8)).cuda()
@@ -69,5 +69,5 @@ for c, nt in itertools.product([int(x) for x in a.clusters.split(",")], [int(x) 
           f"rounds max {pf[:,3].max()}  chol kcyc avg {pf[:,0].mean()/1e3:.1f} max {pf[:,0].max()/1e3:.1f}  "
           f"[Rij {pf[:,6].mean()/1e3:.1f} S {pf[:,7].mean()/1e3:.1f}] jacobi kcyc max {pf[:,1].max()/1e3:.1f}  cyc/round {pf[:,1].max()/max(1,pf[:,3].max()):.0f}  out kcyc {pf[:,2].max()/1e3:.1f}", flush=True)
     R = max(1, pf[:, 3].max())
-    names = ["dot+shfl", "push", "mbar", "pull+red", "params+upd", "ring shfl", "sync", "smem recv+arm"]
+    names = ["dot+push", "mbar wait", "sum", "rot+apply", "ring", "recv", "-", "-"]
     print("   per-round cycles (thread 0):", "  ".join(f"{nm} {ph[:, i].mean()/R:.0f}" for i, nm in enumerate(names)), flush=True)
