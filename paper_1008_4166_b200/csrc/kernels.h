@@ -42,6 +42,7 @@ struct PivotArgs {
   void *Rout;         // optional [count][nmax*nmax]
   int nmax;
   long long *prof;    // optional per-CTA phase clocks [count*C][8] (debug)
+  void *uscr;         // [count][nmax/2][nmax/2+1] factor U of the fast path (L2 scratch)
 };
 // cluster: 0 = automatic choice
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used);

@@ -79,7 +79,8 @@ struct PivCfg {
   static constexpr int SCR0 = HC * NMAX;
   static constexpr int SCR1 = SCR0 > NMAX * RS ? SCR0 : NMAX * RS;  // also the R_final / W slab
   static constexpr bool FAST_OK = NMAX <= 128 && XI * YL <= 32;
-  static constexpr int SCR = (FAST_OK && UB * UL > SCR1) ? UB * UL : SCR1;
+  static constexpr int SCR = SCR1;
+  static constexpr bool U_SMEM = UB * UL <= SCR;  // U staged in Ws for the back substitution
   // shared-memory carve-up (bytes, 16-aligned)
   static constexpr size_t OFF_R = 0;
   static constexpr size_t OFF_W = OFF_R + size_t(NMAX) * RS * sizeof(T);  // scratch / U
@@ -302,7 +303,8 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   // the structured Cholesky (blocking.py:131-134), or herm(B^H B) for the
   // pre-pass (parallel.py:143, core.py:54-55) -- and factors it in a
   // register tile (one CTA barrier per column, no cluster traffic).  The
-  // factor stays in Ws for the back substitution W = R0^-1 R_final.
+  // factor is kept in an L2 scratch (written by CTA 0) for the back
+  // substitution W = R0^-1 R_final.
   bool fast = false;
   const int nt = dense ? 0 : ni;  // rows of R0 with the diagonal sqrt(L_i) block
   const int nu = dense ? N : nj;  // order of U
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         for (int x = 0; x < XI; ++x)
 #pragma unroll
           for (int y = 0; y < YL; ++y) u[x][y] = S<T>::zero();
-        T *scr = Rs;  // staging: HC x NMAX rows of R_ij
+        T *scr = Ws;  // staging: HC x NMAX rows of R_ij
         for (int h0 = 0; h0 < ni; h0 += HC) {
           const int hc = min(HC, ni - h0);
           for (int e = tid; e < HC * nj; e += NT) {
@@ -417,8 +419,12 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         __syncthreads();
       }
       if (chol_ok) {
-        // final factor into Ws: R[k][k] = sqrt(d_k), R[k][l] = U[k][l] / sqrt(d_k)
-        T *U = Ws;
+        // final factor R[k][k] = sqrt(d_k), R[k][l] = U[k][l] / sqrt(d_k):
+        // CTA 0 keeps it in the L2 scratch for the back substitution, every
+        // CTA writes its own rows into the R0 slab
+        T *Ug = reinterpret_cast<T *>(a.uscr) + int64_t(item_id) * Cfg::UB * UL;
+        for (int e = tid; e < NMAX * RS; e += NT) Rs[e] = S<T>::zero();
+        __syncthreads();
 #pragma unroll
         for (int x = 0; x < XI; ++x)
 #pragma unroll
@@ -430,23 +436,19 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
               const double rd = sqrt(piv[i]);
               v = i == l ? scale(S<T>::one(), rd) : divr(u[x][y], rd);
             }
-            U[i + l * UL] = v;
+            if (crank == 0) Ug[i + l * UL] = v;
+            const int g = nt + i;
+            if (g >= row0 && g < row0 + RPC && i <= l && l < nu) Rs[(g - row0) + (nt + l) * RS] = v;
           }
-        __syncthreads();
-        // R0 slab rows of this CTA: [[sqrt(L_i), A / sqrt(L_i)], [0, U]]
-        for (int e = tid; e < NMAX * RS; e += NT) Rs[e] = S<T>::zero();
-        __syncthreads();
+        // rows of the diagonal block: [sqrt(L_i), A / sqrt(L_i)]
         for (int e = tid; e < RPC * NMAX; e += NT) {
           const int gl = e % RPC, c = e / RPC;
           const int g = row0 + gl;
-          if (g >= N || c >= N || c < g) continue;
-          T v;
-          if (g < nt)
-            v = c == g ? scale(S<T>::one(), sqrt(lam[g])) : (c < nt ? S<T>::zero() : divr(A[g + int64_t(c - nt) * bmax], sqrt(lam[g])));
-          else
-            v = U[(g - nt) + (c - nt) * UL];
-          Rs[gl + c * RS] = v;
+          if (g >= nt || c >= N || c < g) continue;
+          Rs[gl + c * RS] = c == g ? scale(S<T>::one(), sqrt(lam[g]))
+                                   : (c < nt ? S<T>::zero() : divr(A[g + int64_t(c - nt) * bmax], sqrt(lam[g])));
         }
+        __threadfence();
         __syncthreads();
         fast = true;
         need_dense = false;
@@ -947,7 +949,11 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       // its lanes holding rows (shuffle broadcast of each solved row).
       constexpr int UL = Cfg::UL, RV = Cfg::RV;
       constexpr int CW = (RPC + NWARP - 1) / NWARP;
-      const T *U = Ws;
+      const T *Ug = reinterpret_cast<const T *>(a.uscr) + int64_t(item_id) * Cfg::UB * UL;  // L2
+      if constexpr (Cfg::U_SMEM) {
+        for (int e = tid; e < Cfg::UB * UL; e += NT) Ws[e] = __ldcg(Ug + e);
+      }
+      const T *U = Cfg::U_SMEM ? Ws : Ug;
       if (in_ring) {
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
@@ -962,7 +968,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         }
       }
       double *rdg = npart;  // 1 / U[k][k]
-      for (int k = tid; k < nu; k += NT) rdg[k] = 1.0 / re(U[k + k * UL]);
+      for (int k = tid; k < nu; k += NT) rdg[k] = 1.0 / re(__ldcg(Ug + k + k * UL));
       __threadfence();
       cluster_sync<C>();
       const int c0 = crank * RPC, c1 = min(N, c0 + RPC);
@@ -992,7 +998,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           for (int v = 0; v < RV; ++v) {
             const int i = lane + 32 * v;
             if (i < k) {
-              const T uik = U[i + k * UL];
+              const T uik = Cfg::U_SMEM ? U[i + k * UL] : __ldcg(U + i + k * UL);
 #pragma unroll
               for (int cc = 0; cc < CW; ++cc) f[cc][v] = sub(f[cc][v], mul(uik, wk[cc]));
             } else if (i == k) {
@@ -1012,8 +1018,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       if (nt > 0) {
         // W_t = F_t / s - (A W_b) / s^2 for this CTA's columns
         T *Wb = Rs;  // [nu][RPC] staging (column stride UL)
-        T *As = Ws;  // A (nt x nu), column stride UL
-        __syncthreads();  // every warp is done with U
+        __syncthreads();
 #pragma unroll
         for (int cc = 0; cc < CW; ++cc)
 #pragma unroll
@@ -1021,10 +1026,6 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
             const int c = cw0 + cc, i = lane + 32 * v;
             if (c < c1 && i < nu) Wb[i + (c - c0) * UL] = f[cc][v];
           }
-        for (int e = tid; e < nt * nu; e += NT) {
-          const int h = e % nt, l = e / nt;
-          As[h + l * UL] = A[h + int64_t(l) * bmax];
-        }
         __syncthreads();
         const int ncol = max(0, c1 - c0);
         for (int e = tid; e < nt * ncol; e += NT) {
@@ -1032,10 +1033,10 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           T acc0 = S<T>::zero(), acc1 = S<T>::zero();
           int l = 0;
           for (; l + 1 < nu; l += 2) {
-            acc0 = add(acc0, mul(As[h + l * UL], Wb[l + cl * UL]));
-            acc1 = add(acc1, mul(As[h + (l + 1) * UL], Wb[(l + 1) + cl * UL]));
+            acc0 = add(acc0, mul(A[h + int64_t(l) * bmax], Wb[l + cl * UL]));
+            acc1 = add(acc1, mul(A[h + int64_t(l + 1) * bmax], Wb[(l + 1) + cl * UL]));
           }
-          if (l < nu) acc0 = add(acc0, mul(As[h + l * UL], Wb[l + cl * UL]));
+          if (l < nu) acc0 = add(acc0, mul(A[h + int64_t(l) * bmax], Wb[l + cl * UL]));
           const double lh = lam[h];
           const T fv = __ldcg(Wout + h + int64_t(c0 + cl) * nmax);
           Wout[h + int64_t(c0 + cl) * nmax] = sub(divr(fv, sqrt(lh)), divr(add(acc0, acc1), lh));
@@ -1203,7 +1204,8 @@ static size_t pivot_smem(bool cx, int nmax, int c) {
   const size_t rs = nmax / c + 1;
   const size_t slab = nmax * rs;
   const size_t ub = nmax / 2;
-  const size_t scr = std::max<size_t>(std::max<size_t>(slab, 16 * nmax), nmax <= 128 ? ub * (ub + 1) : 0);
+  const size_t scr = std::max<size_t>(slab, 16 * nmax);
+  (void)ub;
   return (slab + scr) * w + 2 * c * (nmax / 2) * w + 2 * nmax * w + 3 * nmax * 8 + nmax * 4;
 }
 
@@ -1261,7 +1263,7 @@ static cudaError_t query_clusters(int *out) {
 template <typename T, int NMAX, int C, int NT>
 constexpr bool pivot_allowed() {
 #ifdef HJB_PIVOT_DEV
-  return (S<T>::cx && NMAX == 128 && (C == 4 || C == 8)) || (NMAX == 64 && NT == 256) ||
+  return (S<T>::cx && NMAX == 128 && (C == 4 || C == 8 || C == 16)) || (NMAX == 64 && NT == 256) ||
          (!S<T>::cx && NMAX == 128 && NT == 256 && (C == 2 || C == 4));
 #else
   if (NMAX == 32) return C <= 2 && NT <= 256;

@@ -81,7 +81,7 @@ struct HBuf {
 };
 
 struct Workspace {
-  DBuf G, items, A, Apart, D, Dpart, tickets, W, stats, signs, red, lam, flag;
+  DBuf G, items, A, Apart, D, Dpart, tickets, W, U, stats, signs, red, lam, flag;
   HBuf stats_h, red_h;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> events;
@@ -182,6 +182,7 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   pa.stats = stats_d;
   pa.Rout = Rout;
   pa.nmax = c.nmax;
+  pa.uscr = c.ws->U.p;
   int used = 0;
   CK(launch_pivot(c.cx, pa, c.cluster_req, c.st, &used));
   c.cluster = used;
@@ -218,6 +219,7 @@ int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_co
     CK(cudaMemset(ws.tickets.p, 0, ws.tickets.n));
   }
   CK(ws.W.reserve(size_t(max_count) * nmax * nmax * w));
+  CK(ws.U.reserve(size_t(max_count) * (nmax / 2) * (nmax / 2 + 1) * w));  // pivot factor U (L2 scratch)
   return HJB_OK;
 }
 
@@ -675,6 +677,8 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
   pa.Rout = R_out;
   pa.nmax = nmax;
   pa.prof = g_pivot_prof;
+  CK(ws.U.reserve(size_t(count) * (nmax / 2) * (nmax / 2 + 1) * (dtype == HJB_C128 ? 16 : 8)));
+  pa.uscr = ws.U.p;
   cudaError_t e = launch_pivot(dtype == HJB_C128, pa, cluster, st, nullptr);
   if (e == cudaErrorInvalidConfiguration) return fail(HJB_EINVAL, "hjb_pivot: unsupported cluster size");
   CK(e);

@@ -11,6 +11,7 @@ ap.add_argument("config"); ap.add_argument("--n", type=int); ap.add_argument("--
 ap.add_argument("--clusters", default="4"); ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--threads", default="0")
 ap.add_argument("--count", type=int, default=0, help="limit the number of pivots")
+ap.add_argument("--dup", type=int, default=1, help="tile the pivot list (co-scheduling experiments)")
 ap.add_argument("--sweep", type=int, default=1, help="sweeps run before the timed step")
 a = ap.parse_args()
 kw = {k: v for k, v in (("n", a.n), ("b", a.b)) if v}
@@ -48,6 +49,8 @@ pre = np.array([[off(k), b, 0, 0] for pr in first for k in pr], np.int32)
 W, st, _ = phase(pre)
 _lib.check(L.hjb_update(dt, m, Gd.data_ptr(), m, pre.ctypes.data, pre.shape[0], b, W.data_ptr(), st.data_ptr(), None))
 items = np.array([[off(i), b, off(j), b] for i, j in first], np.int32)
+if a.dup > 1:
+    items = np.ascontiguousarray(np.tile(items, (a.dup, 1)))
 if a.count:
     items = np.ascontiguousarray(items[:a.count])
 import itertools
