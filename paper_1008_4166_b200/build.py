@@ -40,7 +40,23 @@ def nvcc():
     return shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 
 
-def _compile(src, inc, verbose):
+HEADERS = [os.path.join(CSRC, h) for h in ("common.cuh", "kernels.h", "schedule.h")] + [
+    os.path.join(ROOT, "include", "hjb200.h")]
+
+
+def _up_to_date(src, obj, flags):
+    """Incremental: the object is newer than its source and the shared
+    headers, and was built with the same command line."""
+    stamp = obj + ".cmd"
+    if not (os.path.exists(obj) and os.path.exists(stamp)):
+        return False
+    if open(stamp).read() != " ".join(flags):
+        return False
+    t = os.path.getmtime(obj)
+    return all(os.path.getmtime(d) <= t for d in [src] + HEADERS if os.path.exists(d))
+
+
+def _compile(src, inc, verbose, force=False):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     flags = [nvcc(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
              "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", src, "-o", obj]
@@ -51,9 +67,13 @@ def _compile(src, inc, verbose):
             flags += ["-Xptxas", "-v"]
     else:
         flags[1:1] = ["-x", "cu"]
+    if not force and not verbose and _up_to_date(src, obj, flags):
+        return obj, ""
     r = subprocess.run(flags, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    with open(obj + ".cmd", "w") as f:
+        f.write(" ".join(flags))
     return obj, r.stderr
 
 
@@ -73,7 +93,7 @@ def build(force=False, verbose=False):
     inc, lib = nccl_dirs()
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     with cf.ThreadPoolExecutor(len(srcs)) as ex:
-        results = list(ex.map(lambda s: _compile(s, inc, verbose), srcs))
+        results = list(ex.map(lambda s: _compile(s, inc, verbose, force), srcs))
     if verbose:
         for _, log in results:
             sys.stderr.write(log)

@@ -9,8 +9,12 @@
 // Layout: G column-major (ld = ldg); block column = contiguous m x b slab.
 // One CTA computes a TILE x TILE tile of one item's Gram over one K split;
 // operands are staged through shared memory with a cp.async pipeline and fed
-// to mma.sync.m8n8k4.f64 (SASS DMMA).  Split-K partials are reduced by the
-// last-arriving CTA of each tile in fixed split order (deterministic).
+// to mma.sync.m8n8k4.f64 (SASS DMMA).  The K splits of one tile form a
+// thread-block cluster: every CTA parks its partial tile in shared memory and
+// after one cluster barrier reduces a 1/CL slice of the tile over the peers'
+// partials (DSMEM) in fixed rank order -- deterministic and parallel.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -47,7 +51,7 @@ template <> struct GramAcc<cplx> {
   __device__ cplx get(int q) const { return make_double2(r[q], i[q]); }
 };
 
-template <typename T, int WM, int KC, int STAGES, int VEC>
+template <typename T, int WM, int KC, int STAGES, int VEC, int CL>
 __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
     gram_kernel(GramArgs a) {
   using Cfg = GramCfg<T, WM, KC, STAGES>;
@@ -59,8 +63,9 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
   __shared__ int s_last;
 
   const int tiles = a.tiles;
-  const int ti = blockIdx.x / tiles, tj = blockIdx.x % tiles;
-  const int split = blockIdx.y;
+  const int tile_id = blockIdx.x / CL;
+  const int ti = tile_id / tiles, tj = tile_id % tiles;
+  const int split = blockIdx.x % CL;  // == rank in the cluster
   const int item_id = blockIdx.z;
   const Item it = a.items[item_id];
   const bool dense = it.nj == 0;
@@ -146,23 +151,6 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
   }
   cp_async_wait<0>();
 
-  // ---- write this split's partial (or the final value when unsplit) ----
-  const int bmax = a.bmax;
-  const int64_t asz = int64_t(bmax) * bmax;
-  T *Aout = reinterpret_cast<T *>(a.splits > 1 ? a.Apart : a.A) +
-            (a.splits > 1 ? (int64_t(item_id) * a.splits + split) * asz : int64_t(item_id) * asz);
-  double *Dout = a.splits > 1 ? a.Dpart + (int64_t(item_id) * a.splits + split) * 2 * bmax
-                              : a.D + int64_t(item_id) * 2 * bmax;
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int r = ti * TILE + wm * 32 + mi * 8 + (lane >> 2);
-        const int cc = tj * TILE + wn * 32 + ni * 8 + 2 * (lane & 3) + q;
-        if (r < bmax && cc < bmax) Aout[r + int64_t(cc) * bmax] = acc[mi][ni].get(q);
-      }
   // column norms: reduce the 4 lanes holding the same column
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
@@ -171,67 +159,119 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
     dy[mi] += __shfl_xor_sync(0xffffffffu, dy[mi], 1);
     dy[mi] += __shfl_xor_sync(0xffffffffu, dy[mi], 2);
   }
-  if ((lane & 3) == 0) {
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-      const int r = ti * TILE + wm * 32 + mi * 8 + (lane >> 2);
-      if (do_dx && r < bmax) Dout[r] = dx[mi];
-      const int cc = tj * TILE + wn * 32 + mi * 8 + (lane >> 2);
-      if (do_dy && cc < bmax) Dout[bmax + cc] = dy[mi];
-    }
-  }
-  if (a.splits == 1) return;
-
-  // ---- deterministic split-K reduction by the last CTA of this tile ----
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    unsigned *tk = a.tickets + int64_t(item_id) * tiles * tiles + blockIdx.x;
-    const unsigned prev = atomicAdd(tk, 1u);
-    s_last = (prev == unsigned(a.splits - 1));
-    if (s_last) *tk = 0u;  // re-arm for the next launch
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const T *Ap = reinterpret_cast<const T *>(a.Apart) + int64_t(item_id) * a.splits * asz;
+  const int bmax = a.bmax;
+  const int64_t asz = int64_t(bmax) * bmax;
   T *Af = reinterpret_cast<T *>(a.A) + int64_t(item_id) * asz;
-  for (int e = tid; e < TILE * TILE; e += NT) {
-    const int r = ti * TILE + (e % TILE), cc = tj * TILE + (e / TILE);
-    if (r >= bmax || cc >= bmax) continue;
-    const int64_t off = r + int64_t(cc) * bmax;
-    T s = __ldcg(Ap + off);
-    for (int sp = 1; sp < a.splits; ++sp) s = add(s, __ldcg(Ap + sp * asz + off));
-    Af[off] = s;
-  }
-  if (!dense) {
-    const double *Dp = a.Dpart + int64_t(item_id) * a.splits * 2 * bmax;
-    double *Df = a.D + int64_t(item_id) * 2 * bmax;
-    for (int e = tid; e < 2 * TILE; e += NT) {
-      const bool y = e >= TILE;
-      const int idx = (y ? tj : ti) * TILE + (e % TILE);
-      if ((y ? ti != 0 : tj != 0) || idx >= bmax) continue;
-      const int off = (y ? bmax : 0) + idx;
-      double s = __ldcg(Dp + off);
-      for (int sp = 1; sp < a.splits; ++sp) s += __ldcg(Dp + int64_t(sp) * 2 * bmax + off);
-      Df[off] = s;
+  double *Df = a.D + int64_t(item_id) * 2 * bmax;
+  if constexpr (CL == 1) {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = ti * TILE + wm * 32 + mi * 8 + (lane >> 2);
+          const int cc = tj * TILE + wn * 32 + ni * 8 + 2 * (lane & 3) + q;
+          if (r < bmax && cc < bmax) Af[r + int64_t(cc) * bmax] = acc[mi][ni].get(q);
+        }
+    if ((lane & 3) == 0) {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int r = ti * TILE + wm * 32 + mi * 8 + (lane >> 2);
+        if (do_dx && r < bmax) Df[r] = dx[mi];
+        const int cc = tj * TILE + wn * 32 + mi * 8 + (lane >> 2);
+        if (do_dy && cc < bmax) Df[bmax + cc] = dy[mi];
+      }
     }
+  } else {
+    // ---- split-K reduction over the cluster (DSMEM), fixed rank order ----
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    __syncthreads();  // staging buffers are free
+    T *P = smem;                                               // [TILE][TILE] column-major partial
+    double *Pd = reinterpret_cast<double *>(smem + TILE * TILE);  // [2][TILE] norm partials
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = wm * 32 + mi * 8 + (lane >> 2);
+          const int cc = wn * 32 + ni * 8 + 2 * (lane & 3) + q;
+          P[r + cc * TILE] = acc[mi][ni].get(q);
+        }
+    if ((lane & 3) == 0) {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        if (do_dx) Pd[wm * 32 + mi * 8 + (lane >> 2)] = dx[mi];
+        if (do_dy) Pd[TILE + wn * 32 + mi * 8 + (lane >> 2)] = dy[mi];
+      }
+    }
+    cluster.sync();
+    constexpr int E = TILE * TILE, SL = (E + CL - 1) / CL;
+    for (int e = split * SL + tid; e < min(E, (split + 1) * SL); e += NT) {
+      const int r = ti * TILE + (e % TILE), cc = tj * TILE + (e / TILE);
+      T v = *cluster.map_shared_rank(P + e, 0);
+#pragma unroll
+      for (int q = 1; q < CL; ++q) v = add(v, *cluster.map_shared_rank(P + e, q));
+      if (r < bmax && cc < bmax) Af[r + int64_t(cc) * bmax] = v;
+    }
+    if (!dense && split == CL - 1) {
+      for (int e = tid; e < 2 * TILE; e += NT) {
+        const bool y = e >= TILE;
+        const int idx = (y ? tj : ti) * TILE + (e % TILE);
+        if ((y ? ti != 0 : tj != 0) || idx >= bmax) continue;
+        double v = *cluster.map_shared_rank(Pd + e, 0);
+#pragma unroll
+        for (int q = 1; q < CL; ++q) v += *cluster.map_shared_rank(Pd + e, q);
+        Df[(y ? bmax : 0) + idx] = v;
+      }
+    }
+    cluster.sync();  // peers' partials stay alive until every slice is read
   }
 }
 
-template <typename T, int WM, int KC, int STAGES, int VEC>
-static cudaError_t launch_gram_t(const GramArgs &a, cudaStream_t st) {
+template <typename T, int WM, int KC, int STAGES, int VEC, int CL>
+static cudaError_t launch_gram_cl(const GramArgs &a, cudaStream_t st) {
   using Cfg = GramCfg<T, WM, KC, STAGES>;
-  auto k = gram_kernel<T, WM, KC, STAGES, VEC>;
+  static_assert(Cfg::TILE * Cfg::TILE * sizeof(T) + 2 * Cfg::TILE * sizeof(double) <= Cfg::SMEM,
+                "partial tile fits the staging buffers");
+  auto k = gram_kernel<T, WM, KC, STAGES, VEC, CL>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));
     if (e != cudaSuccess) return e;
+    if (CL > 8) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
-  dim3 grid(a.tiles * a.tiles, a.splits, a.count);
-  k<<<grid, Cfg::NT, Cfg::SMEM, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.tiles * a.tiles * CL, 1, a.count);
+  cfg.blockDim = dim3(Cfg::NT);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CL;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+template <typename T, int WM, int KC, int STAGES, int VEC>
+static cudaError_t launch_gram_t(const GramArgs &a, cudaStream_t st) {
+  switch (a.splits) {
+    case 1: return launch_gram_cl<T, WM, KC, STAGES, VEC, 1>(a, st);
+    case 2: return launch_gram_cl<T, WM, KC, STAGES, VEC, 2>(a, st);
+    case 4: return launch_gram_cl<T, WM, KC, STAGES, VEC, 4>(a, st);
+    case 8: return launch_gram_cl<T, WM, KC, STAGES, VEC, 8>(a, st);
+    case 16: return launch_gram_cl<T, WM, KC, STAGES, VEC, 16>(a, st);
+  }
+  return cudaErrorInvalidConfiguration;
 }
 
 int gram_tile(int bmax) { return bmax <= 32 ? 32 : 64; }

@@ -43,6 +43,7 @@ struct PivotArgs {
   int nmax;
   long long *prof;    // optional per-CTA phase clocks [count*C][8] (debug)
   void *uscr;         // [count][nmax/2][nmax/2+1] factor U of the fast path (L2 scratch)
+  void *gchk;         // [count][8][blocks][16] Gram-check partials (L2 scratch), may be null
 };
 // cluster: 0 = automatic choice
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used);
@@ -51,6 +52,7 @@ int pivot_default_cluster(bool cx, int nmax, int count);
 int pivot_default_threads(bool cx, int nmax, int cluster);
 void pivot_tune(int threads, int cluster);  // 0 = automatic
 int pivot_max_active_clusters(bool cx, int nmax, int cluster, int threads);
+size_t pivot_check_elems(int nmax);  // Gram-check scratch elements per item
 
 struct UpdateArgs {
   void *G;

@@ -38,6 +38,11 @@
 namespace cg = cooperative_groups;
 
 // per-round phase clocks (tools/pivot_bench.py); off in production builds
+// a sweep whose largest |t| is below HJB_CHK_SCALE * sqrt(orth_tol) is
+// followed by the one-shot Gram check instead of a ring sweep
+#ifndef HJB_CHK_SCALE
+#define HJB_CHK_SCALE 2.0
+#endif
 #ifndef HJB_ROUND_PROFILE
 #define HJB_ROUND_PROFILE 0
 #endif
@@ -265,6 +270,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   __shared__ int s_big;
   __shared__ int s_fail;
   __shared__ unsigned long long s_maxt;
+  __shared__ unsigned long long s_swt[2];  // per-sweep max |t| (double bits)
   __shared__ uint64_t s_mbar[2];
   __shared__ uint64_t s_pbar[NT / 32];
 
@@ -290,7 +296,10 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     lam[c] = (!dense && c < N) ? a.D[int64_t(item_id) * 2 * bmax + (c < ni ? c : bmax + (c - ni))] : 1.0;
   }
   for (int e = tid; e < NMAX * RS; e += NT) Rs[e] = S<T>::zero();
-  if (tid == 0) { s_fail = INT_MAX; s_maxt = 0ull; s_big = 0; s_cnt[0] = s_cnt[1] = 0; s_flag[0] = 1; }
+  if (tid == 0) {
+    s_fail = INT_MAX; s_maxt = 0ull; s_big = 0; s_cnt[0] = s_cnt[1] = 0; s_flag[0] = 1; s_flag[1] = 0;
+    s_swt[0] = s_swt[1] = 0ull;
+  }
   __syncthreads();
 
   // ------------------------------------------------------------------ R
@@ -668,7 +677,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   int gr = 0;  // exchange counter (mbarrier phases / buffer parities)
   int pg = 0;  // ring-pass counter (pass-buffer parities)
   int my_big = 0, my_cnt = 0, my_fail = INT_MAX;
-  double my_maxt = 0.0;
+  double my_maxt = 0.0, my_swt = 0.0;
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   T *xbuf = reinterpret_cast<T *>(smem + Cfg::OFF_X);             // [2][NWARP][RPC]
   double *xd = reinterpret_cast<double *>(smem + Cfg::OFF_XD);     // [2][NWARP]
@@ -733,9 +742,105 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     return add(d0, d1);
   };
   T dn = dot_part();
+  double prev_swt = 1.0;
+  const double chk_thr = HJB_CHK_SCALE * sqrt(otol);
+  // Gram of the current columns (partials of this CTA's rows, 4 x 4 column
+  // blocks) -> L2 scratch; CTA r checks the blocks b = r mod C against the
+  // skip test; cluster-wide OR of the failures
+  auto gram_check = [&]() -> bool {
+    constexpr int NB = NMAX / 4, NBLK = NB * (NB + 1) / 2;
+    __syncthreads();
+    if (in_ring) {
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int row = lane_in + u * TPP;
+        if (ib - 1 < N) Rs[(ib - 1) * RS + row] = X[u];
+        if (jb - 1 < N) Rs[(jb - 1) * RS + row] = Y[u];
+      }
+    }
+    __syncthreads();
+    T *gs = reinterpret_cast<T *>(a.gchk) + int64_t(item_id) * 8 * NBLK * 16;
+    for (int blk = tid; blk < NBLK; blk += NT) {
+      int R = 0, rem = blk;
+      while (rem >= NB - R) {
+        rem -= NB - R;
+        ++R;
+      }
+      const int Sb = R + rem;
+      T acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = S<T>::zero();
+      if (4 * R < N && 4 * Sb < N) {
+        for (int row = 0; row < RPC; ++row) {
+          T x[4], y[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            x[i] = Rs[(4 * R + i) * RS + row];
+            y[i] = Rs[(4 * Sb + i) * RS + row];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = cfma(x[i], y[j], acc[i][j]);
+        }
+      }
+      T *dst = gs + (int64_t(crank) * NBLK + blk) * 16;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[i * 4 + j] = acc[i][j];
+    }
+    __threadfence();
+    cluster_sync<C>();
+    // fresh column norms (diagonal blocks), summed in rank order
+    double *Dc = npart;
+    for (int c = tid; c < N; c += NT) {
+      const int R = c >> 2, blk = R * NB - R * (R - 1) / 2;  // diagonal block (R, R)
+      double d = 0.0;
+      for (int q = 0; q < C; ++q) d += re(__ldcg(gs + (int64_t(q) * NBLK + blk) * 16 + (c & 3) * 5));
+      Dc[c] = d;
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int e = tid; e < NBLK * 16; e += NT) {
+      const int blk = e >> 4, ij = e & 15;
+      if (blk % C != crank) continue;
+      int R = 0, rem = blk;
+      while (rem >= NB - R) {
+        rem -= NB - R;
+        ++R;
+      }
+      const int r = 4 * R + (ij >> 2), sc = 4 * (R + rem) + (ij & 3);
+      if (r >= sc || sc >= N) continue;
+      T m = S<T>::zero();
+      for (int q = 0; q < C; ++q) m = add(m, __ldcg(gs + (int64_t(q) * NBLK + blk) * 16 + ij));
+      if (!(abs2(m) <= otol2 * (Dc[r] * Dc[sc]))) bad = 1;
+    }
+    bad = __syncthreads_or(bad);
+    if (tid == 0 && bad)
+      for (int q = 0; q < C; ++q) remote<C>(s_flag, q)[1] = 1;
+    cluster_sync<C>();
+    const bool ok = s_flag[1] == 0;
+    __syncthreads();
+    if (tid == 0) s_flag[1] = 0;
+    return ok;
+  };
   if (status == PV_OK) {
     for (int sw = 0; sw < a.max_sweeps; ++sw) {
       ++sweeps;
+      // A sweep after one whose rotations were all tiny is almost surely the
+      // final zero-rotation sweep (rotations.py:220-222): check all its pairs
+      // at once on the Gram matrix of the current columns.  If every pair
+      // passes the skip test of _kernels.py:57 (with D = colnorms^2 at the
+      // sweep start, rotations.py:217) the sweep applies no rotation -- the
+      // same outcome as running it; otherwise run it.
+      if constexpr (Cfg::FAST && C <= 8) {
+        // (pre-pass blocks after the first outer sweep are already
+        // diagonal: check them before their first inner sweep too)
+        if (fast && a.gchk && ((sw > 0 && prev_swt <= chk_thr) || (sw == 0 && dense)) && gram_check()) break;
+      }
       const bool odd = (sw & 1) == 0;  // reference sweeps count from 1; odd send to q-1
       const int src = odd ? (slot + 1 == pr ? 0 : slot + 1) : (slot == 0 ? pr - 1 : slot - 1);
       const int srcw = src / SPW;
@@ -819,6 +924,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
                 const double at = fabs(q.num / q.den);
                 my_big += at > qtol;
                 my_maxt = fmax(my_maxt, at);
+                my_swt = fmax(my_swt, at);
               }
             } else {
               rot = false;
@@ -914,7 +1020,12 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       }
       // sweep end: the rotation count and failures are the same in every
       // CTA (every CTA derived every rotation), so a CTA barrier suffices
-      if (tid == 0) s_cnt[(sw + 1) & 1] = 0;
+      if (tid == 0) {
+        s_cnt[(sw + 1) & 1] = 0;
+        s_swt[(sw + 1) & 1] = 0ull;
+      }
+      if (my_swt > 0.0) atomicMax(&s_swt[sw & 1], static_cast<unsigned long long>(__double_as_longlong(my_swt)));
+      my_swt = 0.0;
       const int wc = __reduce_add_sync(0xffffffffu, my_cnt);
       const int wf = __reduce_min_sync(0xffffffffu, my_fail);
       if (lane == 0) {
@@ -930,6 +1041,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       const int cnt = s_cnt[sw & 1];
       nrot_total += cnt;
       if (cnt == 0) break;
+      prev_swt = __longlong_as_double(static_cast<long long>(s_swt[sw & 1]));
     }
   }
   t_jac = clock64();
@@ -1188,6 +1300,12 @@ static cudaError_t launch_pivot_t(const PivotArgs &a, cudaStream_t st) {
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+size_t pivot_check_elems(int nmax) {
+  if (nmax > 128) return 0;
+  const size_t nb = nmax / 4;
+  return 8 * (nb * (nb + 1) / 2) * 16;  // up to 8 CTAs per cluster on the fast path
 }
 
 int pivot_nmax(int bmax) {

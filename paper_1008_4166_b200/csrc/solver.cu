@@ -81,7 +81,7 @@ struct HBuf {
 };
 
 struct Workspace {
-  DBuf G, items, A, Apart, D, Dpart, tickets, W, U, stats, signs, red, lam, flag;
+  DBuf G, items, A, Apart, D, Dpart, tickets, W, U, Gc, stats, signs, red, lam, flag;
   HBuf stats_h, red_h;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> events;
@@ -116,14 +116,16 @@ Partition uniform_partition(int64_t n, int nbl) {  // blocking.py:63-68
   return P;
 }
 
+// K splits of one Gram tile = the cluster size of gram_kernel (1 .. 16):
+// about two CTAs per SM, at least one K chunk per split
 int gram_splits(int count, int tiles, int64_t m, int kc, int64_t *ksplit) {
   const int64_t chunks = (m + kc - 1) / kc;
-  const int64_t target = 2 * 148;
-  int64_t s = (target + int64_t(count) * tiles * tiles - 1) / (int64_t(count) * tiles * tiles);
-  s = std::max<int64_t>(1, std::min(s, chunks));
+  const int64_t per = int64_t(count) * tiles * tiles;
+  int s = 1;
+  while (s < 16 && per * (2 * s) <= 2 * 148 + per / 2 && 2 * s <= chunks) s *= 2;
   const int64_t cps = (chunks + s - 1) / s;  // chunks per split
   *ksplit = cps * kc;
-  return int((m + *ksplit - 1) / *ksplit);
+  return s;
 }
 
 struct PhaseCtx {
@@ -183,6 +185,7 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   pa.Rout = Rout;
   pa.nmax = c.nmax;
   pa.uscr = c.ws->U.p;
+  pa.gchk = c.ws->Gc.p;
   int used = 0;
   CK(launch_pivot(c.cx, pa, c.cluster_req, c.st, &used));
   c.cluster = used;
@@ -220,6 +223,7 @@ int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_co
   }
   CK(ws.W.reserve(size_t(max_count) * nmax * nmax * w));
   CK(ws.U.reserve(size_t(max_count) * (nmax / 2) * (nmax / 2 + 1) * w));  // pivot factor U (L2 scratch)
+  CK(ws.Gc.reserve(size_t(max_count) * pivot_check_elems(nmax) * w));    // final-sweep Gram check
   return HJB_OK;
 }
 
@@ -679,6 +683,8 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
   pa.prof = g_pivot_prof;
   CK(ws.U.reserve(size_t(count) * (nmax / 2) * (nmax / 2 + 1) * (dtype == HJB_C128 ? 16 : 8)));
   pa.uscr = ws.U.p;
+  CK(ws.Gc.reserve(size_t(count) * pivot_check_elems(nmax) * (dtype == HJB_C128 ? 16 : 8)));
+  pa.gchk = ws.Gc.p;
   cudaError_t e = launch_pivot(dtype == HJB_C128, pa, cluster, st, nullptr);
   if (e == cudaErrorInvalidConfiguration) return fail(HJB_EINVAL, "hjb_pivot: unsupported cluster size");
   CK(e);
