@@ -20,10 +20,15 @@
 
 namespace hjb {
 
+// WM row-warps x 4 column-warps per TILE x TILE tile (TILE = 32 WM); each
+// warp owns 32 rows x TILE/4 columns (NI = TILE/32 8x8 fragments per row
+// block), so every SM keeps 16 warps of DMMA chains in flight
 template <typename T, int WM, int KC, int STAGES>
 struct GramCfg {
   static constexpr int TILE = 32 * WM;
-  static constexpr int NT = 32 * WM * WM;
+  static constexpr int WC = 4;                 // column-warps
+  static constexpr int NI = TILE / (8 * WC);   // 8-column fragments per warp
+  static constexpr int NT = 32 * WM * WC;
   static constexpr int PAD = S<T>::cx ? 4 : 4;
   static constexpr int KCP = KC + PAD;                      // elements per staged column
   static constexpr int STAGE_ELEMS = 2 * TILE * KCP;        // X and Y tiles
@@ -39,16 +44,17 @@ template <> struct GramAcc<double> {
   __device__ double get(int q) const { return v[q]; }
 };
 template <> struct GramAcc<cplx> {
-  double r[2], i[2];
-  __device__ void zero() { r[0] = r[1] = i[0] = i[1] = 0.0; }
+  // four independent DMMA chains (no dependent pair per k step):
+  // conj(a) b = (ar br + ai bi) + i (ar bi - ai br)
+  double rr[2], ii[2], ri[2], ir[2];
+  __device__ void zero() { rr[0] = rr[1] = ii[0] = ii[1] = ri[0] = ri[1] = ir[0] = ir[1] = 0.0; }
   __device__ void mma(cplx a, cplx b) {
-    // conj(a) b = (ar br + ai bi) + i (ar bi - ai br)
-    dmma(r[0], r[1], a.x, b.x);
-    dmma(r[0], r[1], a.y, b.y);
-    dmma(i[0], i[1], a.x, b.y);
-    dmma(i[0], i[1], -a.y, b.x);
+    dmma(rr[0], rr[1], a.x, b.x);
+    dmma(ii[0], ii[1], a.y, b.y);
+    dmma(ri[0], ri[1], a.x, b.y);
+    dmma(ir[0], ir[1], a.y, b.x);
   }
-  __device__ cplx get(int q) const { return make_double2(r[q], i[q]); }
+  __device__ cplx get(int q) const { return make_double2(rr[q] + ii[q], ri[q] - ir[q]); }
 };
 
 template <typename T, int WM, int KC, int STAGES, int VEC, int CL>
@@ -77,8 +83,9 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
   const int nchunks = k1 > k0 ? int((k1 - k0 + KC - 1) / KC) : 0;
   const T *G = reinterpret_cast<const T *>(a.G);
 
+  constexpr int NI = Cfg::NI, WC = Cfg::WC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / WM, wn = warp % WM;
+  const int wm = warp / WC, wn = warp % WC;
 
   auto load_stage = [&](int stage, int chunk) {
     T *Xs = smem + stage * Cfg::STAGE_ELEMS;
@@ -102,12 +109,14 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
     }
   };
 
-  GramAcc<T> acc[4][4];
+  GramAcc<T> acc[4][NI];
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) acc[mi][ni].zero();
-  double dx[4] = {0, 0, 0, 0}, dy[4] = {0, 0, 0, 0};
+    for (int ni = 0; ni < NI; ++ni) acc[mi][ni].zero();
+  double dx[4] = {0, 0, 0, 0}, dy[NI];
+#pragma unroll
+  for (int ni = 0; ni < NI; ++ni) dy[ni] = 0.0;
   const bool do_dx = !dense && tj == 0 && wn == 0;
   const bool do_dy = !dense && ti == 0 && wm == 0;
 
@@ -128,24 +137,24 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
     const T *Ys = Xs + TILE * KCP;
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
-      T fa[4], fb[4];
+      T fa[4], fb[NI];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
         fa[mi] = Xs[(wm * 32 + mi * 8 + (lane >> 2)) * KCP + kk + (lane & 3)];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-        fb[ni] = Ys[(wn * 32 + ni * 8 + (lane >> 2)) * KCP + kk + (lane & 3)];
+      for (int ni = 0; ni < NI; ++ni)
+        fb[ni] = Ys[(wn * 8 * NI + ni * 8 + (lane >> 2)) * KCP + kk + (lane & 3)];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) acc[mi][ni].mma(fa[mi], fb[ni]);
+        for (int ni = 0; ni < NI; ++ni) acc[mi][ni].mma(fa[mi], fb[ni]);
       if (do_dx) {
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) dx[mi] += abs2(fa[mi]);
       }
       if (do_dy) {
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dy[ni] += abs2(fb[ni]);
+        for (int ni = 0; ni < NI; ++ni) dy[ni] += abs2(fb[ni]);
       }
     }
   }
@@ -156,8 +165,11 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
   for (int mi = 0; mi < 4; ++mi) {
     dx[mi] += __shfl_xor_sync(0xffffffffu, dx[mi], 1);
     dx[mi] += __shfl_xor_sync(0xffffffffu, dx[mi], 2);
-    dy[mi] += __shfl_xor_sync(0xffffffffu, dy[mi], 1);
-    dy[mi] += __shfl_xor_sync(0xffffffffu, dy[mi], 2);
+  }
+#pragma unroll
+  for (int ni = 0; ni < NI; ++ni) {
+    dy[ni] += __shfl_xor_sync(0xffffffffu, dy[ni], 1);
+    dy[ni] += __shfl_xor_sync(0xffffffffu, dy[ni], 2);
   }
   const int bmax = a.bmax;
   const int64_t asz = int64_t(bmax) * bmax;
@@ -167,11 +179,11 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int r = ti * TILE + wm * 32 + mi * 8 + (lane >> 2);
-          const int cc = tj * TILE + wn * 32 + ni * 8 + 2 * (lane & 3) + q;
+          const int cc = tj * TILE + wn * 8 * NI + ni * 8 + 2 * (lane & 3) + q;
           if (r < bmax && cc < bmax) Af[r + int64_t(cc) * bmax] = acc[mi][ni].get(q);
         }
     if ((lane & 3) == 0) {
@@ -179,8 +191,11 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
       for (int mi = 0; mi < 4; ++mi) {
         const int r = ti * TILE + wm * 32 + mi * 8 + (lane >> 2);
         if (do_dx && r < bmax) Df[r] = dx[mi];
-        const int cc = tj * TILE + wn * 32 + mi * 8 + (lane >> 2);
-        if (do_dy && cc < bmax) Df[bmax + cc] = dy[mi];
+      }
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const int cc = tj * TILE + wn * 8 * NI + ni * 8 + (lane >> 2);
+        if (do_dy && cc < bmax) Df[bmax + cc] = dy[ni];
       }
     }
   } else {
@@ -193,19 +208,20 @@ __global__ void __launch_bounds__(GramCfg<T, WM, KC, STAGES>::NT)
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int r = wm * 32 + mi * 8 + (lane >> 2);
-          const int cc = wn * 32 + ni * 8 + 2 * (lane & 3) + q;
+          const int cc = wn * 8 * NI + ni * 8 + 2 * (lane & 3) + q;
           P[r + cc * TILE] = acc[mi][ni].get(q);
         }
     if ((lane & 3) == 0) {
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
+      for (int mi = 0; mi < 4; ++mi)
         if (do_dx) Pd[wm * 32 + mi * 8 + (lane >> 2)] = dx[mi];
-        if (do_dy) Pd[TILE + wn * 32 + mi * 8 + (lane >> 2)] = dy[mi];
-      }
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni)
+        if (do_dy) Pd[TILE + wn * 8 * NI + ni * 8 + (lane >> 2)] = dy[ni];
     }
     cluster.sync();
     constexpr int E = TILE * TILE, SL = (E + CL - 1) / CL;
