@@ -3,9 +3,11 @@
 # Usage (under gpurun): bash tools/gpu_round.sh TAG
 TAG=${1:-r1}
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -q --timeout 120 > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
+timeout 900 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/smoke_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "rc=$?" >> gpurun_out/bench_$TAG.err
+timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
+for c in cfg1 cfg3; do timeout 600 python bench.py --config $c --steps 3 --no-cpu-baseline >> gpurun_out/bench_cfgs_$TAG.json 2>> gpurun_out/bench_cfgs_$TAG.err; done
 # launch list of one full cfg2 solve (same kernels as one bench step)
 python tools/profile_solve.py cfg2 > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg2_$TAG.csv python tools/profile_solve.py cfg2 > gpurun_out/ncu_list_$TAG.log 2>&1
