@@ -258,8 +258,12 @@ def main():
     dom = max(kern, key=lambda k: kern[k][0])
     nl = stats["sweeps"] * (1 + steps_per_sweep)
     ach = kern[dom][1] / (kern[dom][0] * 1e-3) / 1e12 if kern[dom][0] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):  # DRAM bytes per launch of this kernel from the committed ncu capture
+        traffic = json.load(open(tp)).get(w.name, {}).get(dom)
     roofline = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak if peak else None, "traffic": None,
+                "frac": ach / peak if peak else None, "traffic": traffic,
                 "per_launch": {"launches": nl, "avg_ms": kern[dom][0] / nl, "flops": kern[dom][1] / nl},
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 tensor/CUDA-core; "
                                "MEASURED_PEAKS.json has no FP64 entry)"}
