@@ -103,6 +103,10 @@ def lib():
                     fn.argtypes = args
                 if L.hjb_version() != 1:
                     raise RuntimeError("libhjb200.so ABI version mismatch")
+                # tuning overrides for experiments (0 = the library's heuristic)
+                nt, cl = int(os.environ.get("HJB_PIVOT_THREADS", 0)), int(os.environ.get("HJB_PIVOT_CLUSTER", 0))
+                if nt or cl:
+                    L.hjb_tune(nt, cl)
                 _lib = L
     return _lib
 

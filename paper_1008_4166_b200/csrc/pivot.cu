@@ -85,7 +85,8 @@ struct PivCfg {
   static constexpr int SCR1 = SCR0 > NMAX * RS ? SCR0 : NMAX * RS;  // also the R_final / W slab
   static constexpr bool FAST_OK = NMAX <= 128 && XI * YL <= 32;
   static constexpr int SCR = SCR1;
-  static constexpr bool U_SMEM = UB * UL <= SCR;  // U staged in Ws for the back substitution
+  // U staged on chip for the back substitution (the contiguous Rs|Ws region)
+  static constexpr bool U_SMEM = UB * UL <= NMAX * RS + SCR;
   // shared-memory carve-up (bytes, 16-aligned)
   static constexpr size_t OFF_R = 0;
   static constexpr size_t OFF_W = OFF_R + size_t(NMAX) * RS * sizeof(T);  // scratch / U
@@ -418,12 +419,14 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
 #pragma unroll
         for (int y = 0; y < YL; ++y) rl[y] = rk[min(tl + TL * y, Cfg::UB - 1)];
 #pragma unroll
-        for (int x = 0; x < XI; ++x)
+        for (int x = 0; x < XI; ++x) {
+          if (ti + TI * x <= k) continue;  // finished rows (whole warps skip late in the factorisation)
 #pragma unroll
           for (int y = 0; y < YL; ++y) {
             const int i = ti + TI * x, l = tl + TL * y;
-            if (i > k && l >= i && l < nu) u[x][y] = cfms(ri[x], rl[y], u[x][y]);
+            if (l >= i && l < nu) u[x][y] = cfms(ri[x], rl[y], u[x][y]);
           }
+        }
         publish(k + 1);
         __syncthreads();
       }
@@ -1063,9 +1066,9 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       constexpr int CW = (RPC + NWARP - 1) / NWARP;
       const T *Ug = reinterpret_cast<const T *>(a.uscr) + int64_t(item_id) * Cfg::UB * UL;  // L2
       if constexpr (Cfg::U_SMEM) {
-        for (int e = tid; e < Cfg::UB * UL; e += NT) Ws[e] = __ldcg(Ug + e);
+        for (int e = tid; e < Cfg::UB * UL; e += NT) Rs[e] = __ldcg(Ug + e);
       }
-      const T *U = Cfg::U_SMEM ? Ws : Ug;
+      const T *U = Cfg::U_SMEM ? Rs : Ug;
       if (in_ring) {
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
