@@ -58,3 +58,15 @@ def signs_to_device(signs, n, device):
     if s.size != n:
         raise ValueError(f"sign vector length {s.size} != column count {n}")
     return torch().from_numpy(s).to(device)
+
+
+def pinned_host_colmajor(m, n, np_dtype):
+    """Fresh m x n column-major numpy array in page-locked host memory
+    (torch's caching host allocator: after the first call the pages are
+    recycled from freed results, so the device->host copy runs at full
+    link speed with no page faults).  The array keeps its storage alive."""
+    import numpy as np
+    t = torch()
+    tdt = {np.dtype(np.float64): t.float64, np.dtype(np.complex128): t.complex128}[np.dtype(np_dtype)]
+    buf = t.empty((n, m), dtype=tdt, pin_memory=True)
+    return buf.numpy().T

@@ -104,10 +104,13 @@ def parallel_jacobi(G, signs, config: SolverConfig):
     A = as_matrix(G)
     m, n = A.shape
     s = as_signs(signs, n)
-    out = np.empty((m, n), dtype=A.dtype, order="F")
     dev = config.device
     if dev is None:
         dev = _device.torch().cuda.current_device() if L.hjb_device_count() > 0 else 0
+    try:  # page-locked result: full-speed D2H (falls back to pageable memory)
+        out = _device.pinned_host_colmajor(m, n, A.dtype)
+    except Exception:
+        out = np.empty((m, n), dtype=A.dtype, order="F")
     pr = _problem(config, m, n, m, np.iscomplexobj(A), _lib.HJB_HOST, A.ctypes.data, out.ctypes.data, s,
                   dev, None)
     rc = L.hjb_solve(C.byref(pr), C.byref(res))
