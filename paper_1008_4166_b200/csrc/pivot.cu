@@ -734,15 +734,10 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
 
   // dot partial of this lane's rows for its slot's current pair
   auto dot_part = [&]() {
-    T d0 = S<T>::zero(), d1 = S<T>::zero();
+    T d[4] = {S<T>::zero(), S<T>::zero(), S<T>::zero(), S<T>::zero()};
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      if (u & 1)
-        d1 = cfma(X[u], Y[u], d1);
-      else
-        d0 = cfma(X[u], Y[u], d0);
-    }
-    return add(d0, d1);
+    for (int u = 0; u < RPT; ++u) d[u & 3] = cfma(X[u], Y[u], d[u & 3]);
+    return add(add(d[0], d[2]), add(d[1], d[3]));
   };
   T dn = dot_part();
   double prev_swt = 1.0;
@@ -899,9 +894,15 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         const int buf = gr & 1;
         mbar_wait_cta(&s_mbar[buf], (gr >> 1) & 1);
         const long long c2 = RCLK();
-        T acc = part[(buf * C) * Cfg::P2 + slot];
+        // pairwise tree over the C partials (same fixed order in every CTA)
+        T pv[C];
 #pragma unroll
-        for (int r = 1; r < C; ++r) acc = add(acc, part[(buf * C + r) * Cfg::P2 + slot]);
+        for (int r = 0; r < C; ++r) pv[r] = part[(buf * C + r) * Cfg::P2 + slot];
+#pragma unroll
+        for (int h = 1; h < C; h <<= 1)
+#pragma unroll
+          for (int r = 0; r + h < C; r += 2 * h) pv[r] = add(pv[r], pv[r + h]);
+        const T acc = pv[0];
         const int ci = ib - 1, cj = jb - 1;
         // skip test first (_kernels.py:57); the rotation parameters are only
         // derived in warps where some pair is not yet orthogonal
@@ -960,7 +961,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         const bool all_j = __all_sync(0xffffffffu, !send_i || !in_ring);
         // one straight-line body per (rotation, moving register) case so the
         // rows software-pipeline: apply -> shuffle -> next dot partial
-        T e0 = S<T>::zero(), e1 = S<T>::zero();
+        T e[4] = {S<T>::zero(), S<T>::zero(), S<T>::zero(), S<T>::zero()};
         auto fused = [&](auto rot_c, auto mode_c) {
           constexpr bool ROT = decltype(rot_c)::value;
           constexpr int MODE = decltype(mode_c)::value;  // 0: X moves, 1: Y moves, 2: per lane
@@ -977,7 +978,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
             if constexpr (MODE == 0) X[u] = nv;
             else if constexpr (MODE == 1) Y[u] = nv;
             else { if (send_i) X[u] = nv; else Y[u] = nv; }
-            if (u & 1) e1 = cfma(X[u], Y[u], e1); else e0 = cfma(X[u], Y[u], e0);
+            e[u & 3] = cfma(X[u], Y[u], e[u & 3]);
           }
         };
         using B1 = std::integral_constant<bool, true>;
@@ -991,7 +992,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         } else {
           if (all_i) fused(B0{}, M0{}); else if (all_j) fused(B0{}, M1{}); else fused(B0{}, M2{});
         }
-        dn = add(e0, e1);
+        dn = add(add(e[0], e[2]), add(e[1], e[3]));
         if (writer) mbar_arrive(&s_pbar[warp]);
         const long long c5 = RCLK();
         if (via_smem) {
