@@ -43,7 +43,7 @@ struct PivotArgs {
   int nmax;
   long long *prof;    // optional per-CTA phase clocks [count*C][8] (debug)
   void *uscr;         // [count][nmax/2][nmax/2+1] factor U of the fast path (L2 scratch)
-  void *gchk;         // [count][8][blocks][16] Gram-check partials (L2 scratch), may be null
+  void *gchk;         // [count][16][blocks][16] Gram-check partials (L2 scratch), may be null
 };
 // cluster: 0 = automatic choice
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used);

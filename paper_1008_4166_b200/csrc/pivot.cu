@@ -43,6 +43,9 @@ namespace cg = cooperative_groups;
 #ifndef HJB_CHK_SCALE
 #define HJB_CHK_SCALE 2.0
 #endif
+#ifndef HJB_ABL_WARPRING
+#define HJB_ABL_WARPRING 0
+#endif
 #ifndef HJB_ROUND_PROFILE
 #define HJB_ROUND_PROFILE 0
 #endif
@@ -752,12 +755,12 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int row = lane_in + u * TPP;
-        if (ib - 1 < N) Rs[(ib - 1) * RS + row] = X[u];
-        if (jb - 1 < N) Rs[(jb - 1) * RS + row] = Y[u];
+        if (ib - 1 < N) Ws[(ib - 1) * RS + row] = X[u];
+        if (jb - 1 < N) Ws[(jb - 1) * RS + row] = Y[u];
       }
     }
     __syncthreads();
-    T *gs = reinterpret_cast<T *>(a.gchk) + int64_t(item_id) * 8 * NBLK * 16;
+    T *gs = reinterpret_cast<T *>(a.gchk) + int64_t(item_id) * 16 * NBLK * 16;
     for (int blk = tid; blk < NBLK; blk += NT) {
       int R = 0, rem = blk;
       while (rem >= NB - R) {
@@ -775,8 +778,8 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           T x[4], y[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            x[i] = Rs[(4 * R + i) * RS + row];
-            y[i] = Rs[(4 * Sb + i) * RS + row];
+            x[i] = Ws[(4 * R + i) * RS + row];
+            y[i] = Ws[(4 * Sb + i) * RS + row];
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -834,17 +837,22 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       // passes the skip test of _kernels.py:57 (with D = colnorms^2 at the
       // sweep start, rotations.py:217) the sweep applies no rotation -- the
       // same outcome as running it; otherwise run it.
-      if constexpr (Cfg::FAST && C <= 8) {
+      {
         // (pre-pass blocks after the first outer sweep are already
         // diagonal: check them before their first inner sweep too)
-        if (fast && a.gchk && ((sw > 0 && prev_swt <= chk_thr) || (sw == 0 && dense)) && gram_check()) break;
+        if (a.gchk && ((sw > 0 && prev_swt <= chk_thr) || (sw == 0 && dense)) && gram_check()) break;
       }
       const bool odd = (sw & 1) == 0;  // reference sweeps count from 1; odd send to q-1
       const int src = odd ? (slot + 1 == pr ? 0 : slot + 1) : (slot == 0 ? pr - 1 : slot - 1);
       const int srcw = src / SPW;
+#if HJB_ABL_WARPRING  // timing ablation only (wrong ordering): the ring wraps inside each warp
+      const bool via_smem = false, writer = false;
+      const int src_lane = (odd ? (wslot + 1) % SPW : (wslot + SPW - 1) % SPW) * TPP + lane_in;
+#else
       const bool via_smem = in_ring && (odd ? (wslot == SPW - 1 || slot == pr - 1) : (wslot == 0 || slot == 0));
       const bool writer = in_ring && (odd ? (wslot == 0) : (wslot == SPW - 1 || slot == pr - 1));
       const int src_lane = odd ? min(lane + TPP, 31) : max(lane - TPP, 0);
+#endif
       // ---- D = colnorms^2(R) (rotations.py:217): cluster-reduced norms ----
       {
         double nx = 0.0, ny = 0.0, nx1 = 0.0, ny1 = 0.0;
@@ -1307,9 +1315,8 @@ static cudaError_t launch_pivot_t(const PivotArgs &a, cudaStream_t st) {
 }
 
 size_t pivot_check_elems(int nmax) {
-  if (nmax > 128) return 0;
   const size_t nb = nmax / 4;
-  return 8 * (nb * (nb + 1) / 2) * 16;  // up to 8 CTAs per cluster on the fast path
+  return 16 * (nb * (nb + 1) / 2) * 16;  // up to 16 CTAs per cluster
 }
 
 int pivot_nmax(int bmax) {
