@@ -156,6 +156,12 @@ int hjb_pivot_set_profile(void *prof);
 /* Tuning override for the pivot kernel: threads per CTA (256/512/1024) and
  * cluster size (1..16); 0 restores the automatic choice. */
 int hjb_tune(int32_t pivot_threads, int32_t pivot_cluster);
+/* Inner pair order of hjb_pivot for (dtype, bmax, count, cluster; 0 = auto):
+ * the warp-block order over *nmax column positions in *warps warps per CTA
+ * (oracle: diagonalize(order="wblock:NMAX:WARPS")).  Replaces nothing in the
+ * reference (its inner order is sequential, _kernels.py:41-52); test hook. */
+int hjb_pivot_order(int32_t dtype, int32_t bmax, int32_t count, int32_t cluster, int32_t *nmax,
+                    int32_t *warps);
 /* Max co-resident clusters of the pivot kernel instance for (dtype, bmax,
  * cluster, threads) on the current device (negative: cudaError). */
 int hjb_pivot_occupancy(int32_t dtype, int32_t bmax, int32_t cluster, int32_t threads);

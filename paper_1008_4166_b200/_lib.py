@@ -73,6 +73,8 @@ SIGNATURES = {
     "hjb_pivot_set_profile": (C.c_int, [C.c_void_p]),
     "hjb_tune": (C.c_int, [C.c_int32, C.c_int32]),
     "hjb_pivot_occupancy": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "hjb_pivot_order": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_int32)]),
     "hjb_update": (C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hjb_exchange_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

@@ -52,7 +52,10 @@ int pivot_default_cluster(bool cx, int nmax, int count);
 int pivot_default_threads(bool cx, int nmax, int cluster);
 void pivot_tune(int threads, int cluster);  // 0 = automatic
 int pivot_max_active_clusters(bool cx, int nmax, int cluster, int threads);
-size_t pivot_check_elems(int nmax);  // Gram-check scratch elements per item
+size_t pivot_check_elems(int nmax);
+// the (cluster, threads) launch_pivot picks when not told (honours hjb_tune)
+int pivot_choose_cluster(bool cx, int nmax, int count);
+int pivot_choose_threads(bool cx, int nmax, int c);  // Gram-check scratch elements per item
 
 struct UpdateArgs {
   void *G;

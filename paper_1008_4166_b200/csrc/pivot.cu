@@ -43,6 +43,9 @@ namespace cg = cooperative_groups;
 #ifndef HJB_CHK_SCALE
 #define HJB_CHK_SCALE 2.0
 #endif
+#ifndef HJB_WBLOCK
+#define HJB_WBLOCK 1
+#endif
 #ifndef HJB_ABL_WARPRING
 #define HJB_ABL_WARPRING 0
 #endif
@@ -277,6 +280,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   __shared__ unsigned long long s_swt[2];  // per-sweep max |t| (double bits)
   __shared__ uint64_t s_mbar[2];
   __shared__ uint64_t s_pbar[NT / 32];
+  __shared__ int s_wbid[HJB_WBLOCK ? NMAX : 1];  // block-step exchange: column ids
 
   int crank = 0;
   if constexpr (C > 1) crank = int(cg::this_cluster().block_rank());
@@ -670,7 +674,10 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   const double otol = a.orth_tol > 0.0 ? a.orth_tol : sqrt(double(N)) * kEps;
   const double otol2 = otol * otol;
   const double qtol = a.quad_tol > 0.0 ? a.quad_tol : double(N) * kEps;
-  const int ne = N + (N & 1);
+  // HJB_WBLOCK: warp-block inner order (oracle WBlockState) over all NMAX
+  // column positions (ids >= N are zero padding that never rotates)
+  constexpr bool WB = HJB_WBLOCK;
+  const int ne = WB ? NMAX : N + (N & 1);
   const int pr = ne / 2;  // ring slots in use
   const int slot = tid / TPP, lane_in = tid % TPP;
   constexpr int SPW = Cfg::SPW, NWARP = Cfg::NWARP;
@@ -678,6 +685,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   const bool in_ring = slot < pr;
   const int wslot = slot % SPW;
   int ip = slot + 1, jp = ne - slot, ib = ip, jb = jp;  // strategies.py:58-66
+  int cX = ib - 1, cY = jb - 1;  // column ids held in X / Y (travel with the data under WB)
   long long nrot_total = 0;
   int sweeps = 0;
   int gr = 0;  // exchange counter (mbarrier phases / buffer parities)
@@ -698,7 +706,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
 #pragma unroll
   for (int u = 0; u < RPT; ++u) {
     const int row = lane_in + u * TPP;
-    const int ci = in_ring ? ib - 1 : 0, cj = in_ring ? jb - 1 : 1;
+    const int ci = in_ring ? cX : 0, cj = in_ring ? cY : 1;
     X[u] = Rs[ci * RS + row];
     Y[u] = Rs[cj * RS + row];
   }
@@ -755,8 +763,8 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int row = lane_in + u * TPP;
-        if (ib - 1 < N) Ws[(ib - 1) * RS + row] = X[u];
-        if (jb - 1 < N) Ws[(jb - 1) * RS + row] = Y[u];
+        if (cX < N) Ws[cX * RS + row] = X[u];
+        if (cY < N) Ws[cY * RS + row] = Y[u];
       }
     }
     __syncthreads();
@@ -849,9 +857,10 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       const bool via_smem = false, writer = false;
       const int src_lane = (odd ? (wslot + 1) % SPW : (wslot + SPW - 1) % SPW) * TPP + lane_in;
 #else
-      const bool via_smem = in_ring && (odd ? (wslot == SPW - 1 || slot == pr - 1) : (wslot == 0 || slot == 0));
-      const bool writer = in_ring && (odd ? (wslot == 0) : (wslot == SPW - 1 || slot == pr - 1));
-      const int src_lane = odd ? min(lane + TPP, 31) : max(lane - TPP, 0);
+      // WB: every column move stays inside the warp (slot q receives from q+1 mod SPW)
+      const bool via_smem = !WB && in_ring && (odd ? (wslot == SPW - 1 || slot == pr - 1) : (wslot == 0 || slot == 0));
+      const bool writer = !WB && in_ring && (odd ? (wslot == 0) : (wslot == SPW - 1 || slot == pr - 1));
+      const int src_lane = WB ? ((wslot + 1) % SPW) * TPP + lane_in : (odd ? min(lane + TPP, 31) : max(lane - TPP, 0));
 #endif
       // ---- D = colnorms^2(R) (rotations.py:217): cluster-reduced norms ----
       {
@@ -884,10 +893,60 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         dY = nn.y;
         ++gr;
       }
-      sX = Jv[min(ib - 1, NMAX - 1)];
-      sY = Jv[min(jb - 1, NMAX - 1)];
+      sX = Jv[min(cX, NMAX - 1)];
+      sY = Jv[min(cY, NMAX - 1)];
+      int lip = wslot + 1, ljp = 2 * SPW - wslot;  // WB phase A: warp-local modulus stepper
 
       for (int rnd = 0; rnd < ne; ++rnd, ++gr, ++pg) {
+        if constexpr (WB) {
+          // phase B block step t (circle method over M = 2 NWARP blocks of
+          // SPW columns; warp i holds pair i): all columns move through
+          // shared memory at the step start, never inside a round
+          const int rb = rnd - 2 * SPW;
+          if (rb >= 0 && rb % SPW == 0) {
+            constexpr int M = 2 * NWARP;
+            const int t = 1 + rb / SPW;
+            auto bpair = [&](int tt, int &bx, int &by) {
+              if (warp == 0) { bx = M - 1; by = tt; }
+              else { bx = (tt + warp) % (M - 1); by = (tt - warp + (M - 1)) % (M - 1); }
+            };
+            int bx, by;
+            bpair(t - 1, bx, by);
+            T *xb = Ws;  // [M * SPW positions][RS]; the padding row carries D
+            __syncthreads();
+            {
+              const int px = bx * SPW + wslot, py = by * SPW + wslot;
+#pragma unroll
+              for (int u = 0; u < RPT; ++u) {
+                xb[px * RS + lane_in + u * TPP] = X[u];
+                xb[py * RS + lane_in + u * TPP] = Y[u];
+              }
+              if (lane_in == 0) {
+                xb[px * RS + RPC] = scale(S<T>::one(), dX);
+                xb[py * RS + RPC] = scale(S<T>::one(), dY);
+                s_wbid[px] = cX;
+                s_wbid[py] = cY;
+              }
+            }
+            __syncthreads();
+            bpair(t, bx, by);
+            {
+              const int px = bx * SPW + wslot, py = by * SPW + wslot;
+#pragma unroll
+              for (int u = 0; u < RPT; ++u) {
+                X[u] = xb[px * RS + lane_in + u * TPP];
+                Y[u] = xb[py * RS + lane_in + u * TPP];
+              }
+              dX = re(xb[px * RS + RPC]);
+              dY = re(xb[py * RS + RPC]);
+              cX = s_wbid[px];
+              cY = s_wbid[py];
+            }
+            sX = Jv[min(cX, NMAX - 1)];
+            sY = Jv[min(cY, NMAX - 1)];
+            dn = dot_part();
+          }
+        }
         const long long c0 = RCLK();
         // (1) CTA partial of g_i^H g_j (computed at the end of the previous
         // round), reduced over the slot's TPP lanes, pushed to the cluster
@@ -911,7 +970,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
 #pragma unroll
           for (int r = 0; r + h < C; r += 2 * h) pv[r] = add(pv[r], pv[r + h]);
         const T acc = pv[0];
-        const int ci = ib - 1, cj = jb - 1;
+        const int ci = cX, cj = cY;
         // skip test first (_kernels.py:57); the rotation parameters are only
         // derived in warps where some pair is not yet orthogonal
         bool rot = in_ring && ci < N && cj < N && !(abs2(acc) <= otol2 * (dX * dY));
@@ -949,18 +1008,39 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         // with nbl = ne: the slot keeps one column and receives the one its
         // neighbour sends; odd sweeps receive from slot+1, strategies.py:69-72)
         // and the next round's dot partial
-        const bool send_i = ip + jp > ne;
-        if (in_ring) {
-          if (send_i) {
-            ++ip;
-            if (ip == jp) {
-              ip -= pr;
-              jp = ip;
+        bool send_i;
+        if constexpr (WB) {
+          // phase A: the modulus stepper inside the warp (nbl = 2 SPW);
+          // phase B: the Y column moves every round
+          send_i = false;
+          if (rnd < 2 * SPW) {
+            send_i = lip + ljp > 2 * SPW;
+            if (send_i) {
+              ++lip;
+              if (lip == ljp) {
+                lip -= SPW;
+                ljp = lip;
+              }
+            } else {
+              ++ljp;
             }
-            ib = ip;
-          } else {
-            ++jp;
-            jb = jp;
+          }
+        } else {
+          send_i = ip + jp > ne;
+          if (in_ring) {
+            if (send_i) {
+              ++ip;
+              if (ip == jp) {
+                ip -= pr;
+                jp = ip;
+              }
+              ib = ip;
+              cX = ib - 1;
+            } else {
+              ++jp;
+              jb = jp;
+              cY = jb - 1;
+            }
           }
         }
         const int par = pg & 1;
@@ -977,6 +1057,11 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           if (writer && lane_in == 0) xd[par * NWARP + warp] = dv;
           const double nd = __shfl_sync(0xffffffffu, dv, src_lane);
           if (MODE == 0 || (MODE == 2 && send_i)) dX = nd; else dY = nd;
+          if constexpr (WB) {  // the column id travels with the column
+            const int cv = MODE == 0 ? cX : (MODE == 1 ? cY : (send_i ? cX : cY));
+            const int nc = __shfl_sync(0xffffffffu, cv, src_lane);
+            if (MODE == 0 || (MODE == 2 && send_i)) cX = nc; else cY = nc;
+          }
 #pragma unroll
           for (int u = 0; u < RPT; ++u) {
             if constexpr (ROT) rot_fold<T>(X[u], Y[u], p);
@@ -1021,8 +1106,8 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           dn = dot_part();
         }
         // J signs of the slot's (possibly new) columns (static per column)
-        sX = Jv[min(ib - 1, NMAX - 1)];
-        sY = Jv[min(jb - 1, NMAX - 1)];
+        sX = Jv[min(cX, NMAX - 1)];
+        sY = Jv[min(cY, NMAX - 1)];
         __syncwarp();
         const long long c6 = RCLK();
         if (HJB_ROUND_PROFILE && a.prof) {
@@ -1083,11 +1168,11 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         for (int u = 0; u < RPT; ++u) {
           const int g = row0 + lane_in + u * TPP;
           if (g >= N) continue;
-          if (ib - 1 < N) Wout[g + int64_t(ib - 1) * nmax] = X[u];
-          if (jb - 1 < N) Wout[g + int64_t(jb - 1) * nmax] = Y[u];
+          if (cX < N) Wout[g + int64_t(cX) * nmax] = X[u];
+          if (cY < N) Wout[g + int64_t(cY) * nmax] = Y[u];
           if (Rout) {
-            if (ib - 1 < N) Rout[g + int64_t(ib - 1) * nmax] = X[u];
-            if (jb - 1 < N) Rout[g + int64_t(jb - 1) * nmax] = Y[u];
+            if (cX < N) Rout[g + int64_t(cX) * nmax] = X[u];
+            if (cY < N) Rout[g + int64_t(cY) * nmax] = Y[u];
           }
         }
       }
@@ -1175,8 +1260,8 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     for (int u = 0; u < RPT; ++u) {
       if (!in_ring) break;
       const int row = lane_in + u * TPP;
-      Fs[(ib - 1) * RS + row] = X[u];
-      Fs[(jb - 1) * RS + row] = Y[u];
+      Fs[cX * RS + row] = X[u];
+      Fs[cY * RS + row] = Y[u];
     }
     __syncthreads();
     for (int k = C - 1; k >= 0; --k) {
@@ -1467,6 +1552,14 @@ int pivot_default_threads(bool cx, int nmax, int c) {
     if (rpc / tpp <= cap) return nt;
   }
   return 512;
+}
+
+int pivot_choose_cluster(bool cx, int nmax, int count) {
+  return g_tune_cluster > 0 ? g_tune_cluster : pivot_default_cluster(cx, nmax, count);
+}
+
+int pivot_choose_threads(bool cx, int nmax, int c) {
+  return g_tune_threads > 0 ? g_tune_threads : pivot_default_threads(cx, nmax, c);
 }
 
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used) {

@@ -346,6 +346,17 @@ int hjb_pivot_set_profile(void *prof) {
   return HJB_OK;
 }
 
+int hjb_pivot_order(int32_t dtype, int32_t bmax, int32_t count, int32_t cluster, int32_t *nmax,
+                    int32_t *warps) {
+  const bool cx = dtype == HJB_C128;
+  const int nm = pivot_nmax(bmax);
+  if (nm < 0 || count < 1) return HJB_EINVAL;
+  const int c = cluster > 0 ? cluster : pivot_choose_cluster(cx, nm, count);
+  *nmax = nm;
+  *warps = pivot_choose_threads(cx, nm, c) / 32;
+  return HJB_OK;
+}
+
 int hjb_pivot_occupancy(int32_t dtype, int32_t bmax, int32_t cluster, int32_t threads) {
   return pivot_max_active_clusters(dtype == HJB_C128, pivot_nmax(bmax), cluster, threads);
 }
