@@ -692,6 +692,9 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   int pg = 0;  // ring-pass counter (pass-buffer parities)
   int my_big = 0, my_cnt = 0, my_fail = INT_MAX;
   double my_maxt = 0.0, my_swt = 0.0;
+  // max |t| = num/den kept as a fraction (compared by cross-multiplication,
+  // divided once per sweep) so no division sits before the apply loop
+  double mt_n = 0.0, mt_d = 1.0, sw_n = 0.0, sw_d = 1.0;
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   T *xbuf = reinterpret_cast<T *>(smem + Cfg::OFF_X);             // [2][NWARP][RPC]
   double *xd = reinterpret_cast<double *>(smem + Cfg::OFF_XD);     // [2][NWARP]
@@ -848,7 +851,11 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
       {
         // (pre-pass blocks after the first outer sweep are already
         // diagonal: check them before their first inner sweep too)
-        if (a.gchk && ((sw > 0 && prev_swt <= chk_thr) || (sw == 0 && dense)) && gram_check()) break;
+        const long long cg0 = RCLK();
+        const bool gc_try = a.gchk && ((sw > 0 && prev_swt <= chk_thr) || (sw == 0 && dense));
+        const bool gc_ok = gc_try && gram_check();
+        if (HJB_ROUND_PROFILE && a.prof) ph[7] += RCLK() - cg0;
+        if (gc_ok) break;
       }
       const bool odd = (sw & 1) == 0;  // reference sweeps count from 1; odd send to q-1
       const int src = odd ? (slot + 1 == pr ? 0 : slot + 1) : (slot == 0 ? pr - 1 : slot - 1);
@@ -904,6 +911,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
           // shared memory at the step start, never inside a round
           const int rb = rnd - 2 * SPW;
           if (rb >= 0 && rb % SPW == 0) {
+            const long long cx0 = RCLK();
             constexpr int M = 2 * NWARP;
             const int t = 1 + rb / SPW;
             auto bpair = [&](int tt, int &bx, int &by) {
@@ -945,6 +953,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
             sX = Jv[min(cX, NMAX - 1)];
             sY = Jv[min(cY, NMAX - 1)];
             dn = dot_part();
+            if (HJB_ROUND_PROFILE && a.prof) ph[6] += RCLK() - cx0;
           }
         }
         const long long c0 = RCLK();
@@ -981,21 +990,23 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         p.hs = 0.0;
         p.cs = 1.0;
         const long long c3 = RCLK();
+        // D update (_kernels.py:80-81) te = t eta, t = num/den: its division
+        // is done after the apply loop (dX/dY are not needed before)
+        double te_n = 0.0, te_d = 1.0, te_h = 0.0;
         if (any_rot) {
           if (rot) {
             const RotCoef<T> q = rot_coef<T>(acc, dX, dY, sX == sY, otol2);
             if (q.code == 1) {
               p = q;
-              // D update (_kernels.py:80-81), off the dependency chain
-              const double te = q.num * q.eta / q.den;
-              dX = fma(q.hyp, te, dX);
-              dY = dY + te;
+              te_n = q.num * q.eta;
+              te_d = q.den;
+              te_h = q.hyp;
               if (lane_in == 0) {
                 ++my_cnt;
-                const double at = fabs(q.num / q.den);
-                my_big += at > qtol;
-                my_maxt = fmax(my_maxt, at);
-                my_swt = fmax(my_swt, at);
+                const double an = fabs(q.num);
+                my_big += an > qtol * q.den;  // |t| > quad_tol
+                if (an * mt_d > mt_n * q.den) { mt_n = an; mt_d = q.den; }
+                if (an * sw_d > sw_n * q.den) { sw_n = an; sw_d = q.den; }
               }
             } else {
               rot = false;
@@ -1053,15 +1064,6 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         auto fused = [&](auto rot_c, auto mode_c) {
           constexpr bool ROT = decltype(rot_c)::value;
           constexpr int MODE = decltype(mode_c)::value;  // 0: X moves, 1: Y moves, 2: per lane
-          const double dv = MODE == 0 ? dX : (MODE == 1 ? dY : (send_i ? dX : dY));
-          if (writer && lane_in == 0) xd[par * NWARP + warp] = dv;
-          const double nd = __shfl_sync(0xffffffffu, dv, src_lane);
-          if (MODE == 0 || (MODE == 2 && send_i)) dX = nd; else dY = nd;
-          if constexpr (WB) {  // the column id travels with the column
-            const int cv = MODE == 0 ? cX : (MODE == 1 ? cY : (send_i ? cX : cY));
-            const int nc = __shfl_sync(0xffffffffu, cv, src_lane);
-            if (MODE == 0 || (MODE == 2 && send_i)) cX = nc; else cY = nc;
-          }
 #pragma unroll
           for (int u = 0; u < RPT; ++u) {
             if constexpr (ROT) rot_fold<T>(X[u], Y[u], p);
@@ -1072,6 +1074,21 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
             else if constexpr (MODE == 1) Y[u] = nv;
             else { if (send_i) X[u] = nv; else Y[u] = nv; }
             e[u & 3] = cfma(X[u], Y[u], e[u & 3]);
+          }
+          if constexpr (ROT) {
+            const double te = te_n / te_d;
+            dX = fma(te_h, te, dX);
+            dY = dY + te;
+          }
+          // the moving column's D value (and id) follow it
+          const double dv = MODE == 0 ? dX : (MODE == 1 ? dY : (send_i ? dX : dY));
+          if (writer && lane_in == 0) xd[par * NWARP + warp] = dv;
+          const double nd = __shfl_sync(0xffffffffu, dv, src_lane);
+          if (MODE == 0 || (MODE == 2 && send_i)) dX = nd; else dY = nd;
+          if constexpr (WB) {
+            const int cv = MODE == 0 ? cX : (MODE == 1 ? cY : (send_i ? cX : cY));
+            const int nc = __shfl_sync(0xffffffffu, cv, src_lane);
+            if (MODE == 0 || (MODE == 2 && send_i)) cX = nc; else cY = nc;
           }
         };
         using B1 = std::integral_constant<bool, true>;
@@ -1121,8 +1138,11 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         s_cnt[(sw + 1) & 1] = 0;
         s_swt[(sw + 1) & 1] = 0ull;
       }
+      my_swt = sw_n / sw_d;
       if (my_swt > 0.0) atomicMax(&s_swt[sw & 1], static_cast<unsigned long long>(__double_as_longlong(my_swt)));
       my_swt = 0.0;
+      sw_n = 0.0;
+      sw_d = 1.0;
       const int wc = __reduce_add_sync(0xffffffffu, my_cnt);
       const int wf = __reduce_min_sync(0xffffffffu, my_fail);
       if (lane == 0) {
@@ -1145,6 +1165,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
 
   // ------------------------------------------------------------------ W = R0^-1 R
   if (my_big) atomicAdd(&s_big, my_big);
+  my_maxt = mt_n / mt_d;
   if (my_maxt > 0.0) atomicMax(&s_maxt, static_cast<unsigned long long>(__double_as_longlong(my_maxt)));
   const int nmax = a.nmax;
   T *Wout = reinterpret_cast<T *>(a.W) + int64_t(item_id) * nmax * nmax;
@@ -1436,6 +1457,7 @@ int pivot_default_cluster(bool cx, int nmax, int count) {
   int best = cmin;
   for (int c = cmin; c <= 16; c *= 2) {
     if (nmax / c < 16 && c > cmin) break;
+    if (nmax <= 128 && c > 4 && c > cmin) break;  // cfg2: 4 x 256 beats 8 x 128 (profiles/r1_v8_pivot_bench_cfg2.log)
     const int ci = c == 1 ? 0 : c == 2 ? 1 : c == 4 ? 2 : c == 8 ? 3 : 4;
     const int nt = pivot_default_threads(cx, nmax, c);
     int &occ = cache[cx][ni][ci];

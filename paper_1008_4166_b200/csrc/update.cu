@@ -10,6 +10,13 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef HJB_UPD_R256_MT  // rows per CTA of the N_max = 256 update (real / complex)
+#define HJB_UPD_R256_MT 32
+#endif
+#ifndef HJB_UPD_C256_MT
+#define HJB_UPD_C256_MT 16
+#endif
+
 namespace hjb {
 
 template <typename T, int NMAX, int MT, int KW>
@@ -24,6 +31,11 @@ struct UpdCfg {
   static constexpr int WSZ = NMAX * KWP;       // W stage elements ([col][k])
   static constexpr int STAGE = XS + WSZ;
   static constexpr size_t SMEM = 2 * size_t(STAGE) * sizeof(T);
+  // N_max = 256: short row tiles (32 real / 16 complex rows) with 2 CTAs per
+  // SM, so 16 warps keep DMMA chains in flight: 1 CTA of 8 warps with 64/32
+  // rows ran the tensor pipe at ~65 % (tools/upd_bench.py: cfg5r shape 24.2 ->
+  // 29.5 TFLOP/s, cfg5c shape 25.6 -> 31.4 TFLOP/s)
+  static constexpr int MINB = (NMAX == 256 && MI * NI * (S<T>::cx ? 4 : 2) <= 32 && 2 * SMEM <= 227 * 1024) ? 2 : 1;
   static_assert(NI >= 1, "at least one MMA tile per warp");
 };
 
@@ -48,7 +60,7 @@ template <> struct UpdAcc<cplx> {
 };
 
 template <typename T, int NMAX, int MT, int KW, int VEC>
-__global__ void __launch_bounds__(256) update_kernel(UpdateArgs a) {
+__global__ void __launch_bounds__(256, (UpdCfg<T, NMAX, MT, KW>::MINB)) update_kernel(UpdateArgs a) {
   using Cfg = UpdCfg<T, NMAX, MT, KW>;
   constexpr int NT = Cfg::NT, NW = Cfg::NW, NI = Cfg::NI, MI = Cfg::MI;
   constexpr int MTP = Cfg::MTP, KWP = Cfg::KWP;
@@ -160,7 +172,7 @@ cudaError_t launch_update(bool cx, const UpdateArgs &a, cudaStream_t st) {
       case 32:  // W keeps ld = nmax; columns >= N are zero-filled
       case 64: return launch_update_t<cplx, 64, 64, 8, 16>(a, st);
       case 128: return launch_update_t<cplx, 128, 32, 8, 16>(a, st);
-      case 256: return launch_update_t<cplx, 256, 32, 8, 16>(a, st);
+      case 256: return launch_update_t<cplx, 256, HJB_UPD_C256_MT, 8, 16>(a, st);
     }
   } else {
     const bool v16 = a.ldg % 2 == 0;
@@ -168,7 +180,8 @@ cudaError_t launch_update(bool cx, const UpdateArgs &a, cudaStream_t st) {
       case 32:
       case 64: return v16 ? launch_update_t<double, 64, 128, 16, 16>(a, st) : launch_update_t<double, 64, 128, 16, 8>(a, st);
       case 128: return v16 ? launch_update_t<double, 128, 64, 16, 16>(a, st) : launch_update_t<double, 128, 64, 16, 8>(a, st);
-      case 256: return v16 ? launch_update_t<double, 256, 64, 16, 16>(a, st) : launch_update_t<double, 256, 64, 16, 8>(a, st);
+      case 256: return v16 ? launch_update_t<double, 256, HJB_UPD_R256_MT, 16, 16>(a, st)
+                           : launch_update_t<double, 256, HJB_UPD_R256_MT, 16, 8>(a, st);
     }
   }
   return cudaErrorInvalidValue;

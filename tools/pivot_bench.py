@@ -72,5 +72,5 @@ for c, nt in itertools.product([int(x) for x in a.clusters.split(",")], [int(x) 
           f"rounds max {pf[:,3].max()}  chol kcyc avg {pf[:,0].mean()/1e3:.1f} max {pf[:,0].max()/1e3:.1f}  "
           f"[Rij {pf[:,6].mean()/1e3:.1f} S {pf[:,7].mean()/1e3:.1f}] jacobi kcyc max {pf[:,1].max()/1e3:.1f}  cyc/round {pf[:,1].max()/max(1,pf[:,3].max()):.0f}  out kcyc {pf[:,2].max()/1e3:.1f}", flush=True)
     R = max(1, pf[:, 3].max())
-    names = ["dot+push", "mbar wait", "sum", "rot+apply", "ring", "recv", "-", "-"]
+    names = ["dot+push", "mbar wait", "sum", "rot+apply", "ring", "recv", "blkxchg", "gramchk"]
     print("   per-round cycles (thread 0):", "  ".join(f"{nm} {ph[:, i].mean()/R:.0f}" for i, nm in enumerate(names)), flush=True)
