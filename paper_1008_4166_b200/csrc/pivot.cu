@@ -1457,7 +1457,6 @@ int pivot_default_cluster(bool cx, int nmax, int count) {
   int best = cmin;
   for (int c = cmin; c <= 16; c *= 2) {
     if (nmax / c < 16 && c > cmin) break;
-    if (nmax <= 128 && c > 4 && c > cmin) break;  // cfg2: 4 x 256 beats 8 x 128 (profiles/r1_v8_pivot_bench_cfg2.log)
     const int ci = c == 1 ? 0 : c == 2 ? 1 : c == 4 ? 2 : c == 8 ? 3 : 4;
     const int nt = pivot_default_threads(cx, nmax, c);
     int &occ = cache[cx][ni][ci];

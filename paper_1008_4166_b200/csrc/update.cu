@@ -35,7 +35,7 @@ struct UpdCfg {
   // SM, so 16 warps keep DMMA chains in flight: 1 CTA of 8 warps with 64/32
   // rows ran the tensor pipe at ~65 % (tools/upd_bench.py: cfg5r shape 24.2 ->
   // 29.5 TFLOP/s, cfg5c shape 25.6 -> 31.4 TFLOP/s)
-  static constexpr int MINB = (NMAX == 256 && MI * NI * (S<T>::cx ? 4 : 2) <= 32 && 2 * SMEM <= 227 * 1024) ? 2 : 1;
+  static constexpr int MINB = (2 * SMEM <= 227 * 1024) ? 2 : 1;  // (an explicit 1 lets ptxas take >128 registers)
   static_assert(NI >= 1, "at least one MMA tile per warp");
 };
 
