@@ -120,6 +120,15 @@ int hjb_extract(int32_t dtype, int64_t m, int64_t n, const void *G, int64_t ldg,
                 const int8_t *signs_dev, double *lam, void *U, int64_t ldu,
                 const int64_t *perm, void *stream);
 
+/*
+ * Orthogonality metric of solve.py:108-110 on device: *out = max |U^H U - I|
+ * over all entries (host double).  U is a device m x n matrix, ld ldu (even
+ * for float64).  Formed with the Gram kernel over all 64-column block pairs
+ * (i <= j) and a max-fold kernel; replaces the host O(m n^2) product.
+ */
+int hjb_orthogonality(int32_t dtype, int64_t m, int64_t n, const void *U, int64_t ldu, double *out,
+                      void *stream);
+
 /* ---- kernel-level entry points (device pointers), used by parity tests ---- */
 
 /*

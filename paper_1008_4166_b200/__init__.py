@@ -19,7 +19,7 @@ from .errors import (
 from .factorization import (FactoredForm, accept_external_factor, factorize_hermitian_indefinite,
                             order_by_inertia, scaled_condition)
 from .parallel import SolverConfig, parallel_jacobi
-from .rotations import DiagInfo, Tolerances, extract_eigen
+from .rotations import DiagInfo, Tolerances, extract_eigen, orthogonality
 from .solve import SolveOptions, run_solver, solve_hermitian
 from .strategies import MODULUS, ROUND_ROBIN, generate_sweep_schedule, normalize_strategy, steps_per_sweep
 
@@ -29,7 +29,7 @@ __all__ = [
     "BlockPartition", "ChannelTimeoutError", "DefinitenessError", "DiagInfo", "EigenResult",
     "HJacobiError", "MODULUS", "NonConvergenceError", "PivotDefinitenessError", "ROUND_ROBIN",
     "RankDeficiencyError", "SingularMatrixError", "SolverConfig", "StructuralError", "Tolerances",
-    "as_matrix", "as_signs", "extract_eigen", "generate_sweep_schedule", "greedy_partition",
+    "as_matrix", "as_signs", "extract_eigen", "orthogonality", "generate_sweep_schedule", "greedy_partition",
     "normalize_strategy", "num_blocks", "parallel_jacobi", "steps_per_sweep", "uniform_partition",
     "FactoredForm", "accept_external_factor", "factorize_hermitian_indefinite", "order_by_inertia",
     "scaled_condition", "SolveOptions", "run_solver", "solve_hermitian",

@@ -64,6 +64,8 @@ SIGNATURES = {
     "hjb_steps_per_sweep": (C.c_int, [C.c_int32, C.c_int32]),
     "hjb_extract": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "hjb_orthogonality": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                    C.POINTER(C.c_double), C.c_void_p]),
     "hjb_gram": (C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
                            C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hjb_pivot": (C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,

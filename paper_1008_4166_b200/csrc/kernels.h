@@ -72,4 +72,7 @@ cudaError_t launch_extract(bool cx, int64_t m, int64_t n, const void *G, int64_t
                            const int8_t *signs, double *lam, void *U, int64_t ldu,
                            const int64_t *perm, int *zero_flag, cudaStream_t st);
 
+cudaError_t launch_orth_max(bool cx, const Item *items, int count, int bmax, const void *A,
+                            unsigned long long *out, cudaStream_t st);
+
 }  // namespace hjb

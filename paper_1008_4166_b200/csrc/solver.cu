@@ -745,4 +745,61 @@ int hjb_extract(int32_t dtype, int64_t m, int64_t n, const void *G, int64_t ldg,
   return HJB_OK;
 }
 
+int hjb_orthogonality(int32_t dtype, int64_t m, int64_t n, const void *U, int64_t ldu, double *out,
+                      void *stream) {
+  if (m < 1 || n < 0 || !U || !out || ldu < m) return fail(HJB_EINVAL, "hjb_orthogonality: bad arguments");
+  if (dtype != HJB_C128 && (ldu & 1)) return fail(HJB_EINVAL, "hjb_orthogonality: ldu must be even for float64");
+  *out = 0.0;
+  if (n == 0) return HJB_OK;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  Workspace &ws = g_ws[dev];
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool cx = dtype == HJB_C128;
+  // column blocks of width 64; every block pair (i <= j) is one Gram item
+  const int bw = 64;
+  const int nbl = int((n + bw - 1) / bw);
+  std::vector<Item> all;
+  all.reserve(size_t(nbl) * (nbl + 1) / 2);
+  for (int i = 0; i < nbl; ++i)
+    for (int j = i; j < nbl; ++j) {
+      const int oi = i * bw, oj = j * bw;
+      all.push_back(Item{oi, int(std::min<int64_t>(bw, n - oi)), oj, int(std::min<int64_t>(bw, n - oj))});
+    }
+  const int chunk = int(std::min<size_t>(all.size(), 4096));
+  if (int rc = reserve_phase_buffers(ws, cx, bw, 64, chunk, m)) return rc;
+  CK(ws.items.reserve(all.size() * sizeof(Item)));
+  CK(cudaMemcpyAsync(ws.items.p, all.data(), all.size() * sizeof(Item), cudaMemcpyHostToDevice, st));
+  CK(ws.red.reserve(sizeof(unsigned long long)));
+  unsigned long long *acc = static_cast<unsigned long long *>(ws.red.p);
+  CK(cudaMemsetAsync(acc, 0, sizeof(unsigned long long), st));
+  const int tile = gram_tile(bw);
+  const int tiles = (bw + tile - 1) / tile;
+  for (size_t s0 = 0; s0 < all.size(); s0 += chunk) {
+    const int count = int(std::min<size_t>(chunk, all.size() - s0));
+    const Item *items_d = static_cast<const Item *>(ws.items.p) + s0;
+    GramArgs g{};
+    g.G = U;
+    g.ldg = ldu;
+    g.m = m;
+    g.items = items_d;
+    g.count = count;
+    g.bmax = bw;
+    g.splits = gram_splits(count, tiles, m, gram_kc(cx), &g.ksplit);
+    g.Apart = ws.Apart.p;
+    g.Dpart = static_cast<double *>(ws.Dpart.p);
+    g.A = ws.A.p;
+    g.D = static_cast<double *>(ws.D.p);
+    g.tickets = static_cast<unsigned *>(ws.tickets.p);
+    CK(launch_gram(cx, g, st));
+    CK(launch_orth_max(cx, items_d, count, bw, ws.A.p, acc, st));
+  }
+  unsigned long long bits = 0;
+  CK(cudaMemcpyAsync(&bits, acc, sizeof(bits), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::memcpy(out, &bits, sizeof(double));
+  return HJB_OK;
+}
+
 }  // extern "C"

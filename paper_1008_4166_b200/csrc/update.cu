@@ -231,4 +231,53 @@ cudaError_t launch_extract(bool cx, int64_t m, int64_t n, const void *G, int64_t
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- orthogonality
+// solve.py:108-110: max |U^H U - I|.  A holds the Gram tiles of a batch of
+// block pairs (gram_kernel, items with oi <= oj); each CTA folds one tile and
+// the maximum goes to *out as the bit pattern of a non-negative double
+// (ordered like unsigned integers, so atomicMax is exact; a NaN wins).
+template <typename T>
+__global__ void __launch_bounds__(256) orth_max_kernel(const Item *items, int bmax, const T *A,
+                                                      unsigned long long *out) {
+  const Item it = items[blockIdx.x];
+  const T *a = A + size_t(blockIdx.x) * bmax * bmax;
+  double v = 0.0;
+  for (int e = threadIdx.x; e < it.ni * it.nj; e += blockDim.x) {
+    const int r = e % it.ni, c = e / it.ni;
+    T x = a[size_t(c) * bmax + r];
+    double d;
+    if constexpr (sizeof(T) == 16) {
+      if (it.oi + r == it.oj + c) x.x -= 1.0;
+      d = sqrt(abs2(x));
+    } else {
+      if (it.oi + r == it.oj + c) x -= 1.0;
+      d = fabs(x);
+    }
+    v = (d > v || d != d) ? d : v;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double o = red[threadIdx.x + w];
+      if (o > red[threadIdx.x] || o != o) red[threadIdx.x] = o;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(red[0])));
+}
+
+cudaError_t launch_orth_max(bool cx, const Item *items, int count, int bmax, const void *A,
+                            unsigned long long *out, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  if (cx)
+    orth_max_kernel<cplx><<<unsigned(count), 256, 0, st>>>(items, bmax, reinterpret_cast<const cplx *>(A), out);
+  else
+    orth_max_kernel<double><<<unsigned(count), 256, 0, st>>>(items, bmax, reinterpret_cast<const double *>(A),
+                                                            out);
+  return cudaGetLastError();
+}
+
 }  // namespace hjb

@@ -99,3 +99,26 @@ def extract_eigen(G_final, signs, col_perm=None, sort_descending=False):
     if host:
         return EigenResult(eigenvalues=lam.cpu().numpy(), eigenvectors=_device.to_host(U))
     return EigenResult(eigenvalues=lam, eigenvectors=U)
+
+
+def orthogonality(U):
+    """max |U^H U - I| (the reference's ``orthogonality`` metric, solve.py:
+    108-110) on the GPU through hjb_orthogonality (Gram kernel over all
+    64-column block pairs + a max fold).  ``U`` is a host array or CUDA tensor."""
+    import ctypes
+
+    torch = _device.torch()
+    Ud, m, n = _device.as_device_colmajor(U)
+    if m == 0 or n == 0:
+        return 0.0
+    ld = m
+    if not Ud.is_complex() and m % 2:
+        # 16-byte aligned columns for the Gram kernel's cp.async staging
+        P = torch.zeros((n, m + 1), dtype=Ud.dtype, device=Ud.device)
+        P[:, :m] = Ud.t()
+        Ud, ld = P.t(), m + 1
+    dt = _lib.HJB_C128 if Ud.is_complex() else _lib.HJB_F64
+    out = ctypes.c_double(0.0)
+    st = torch.cuda.current_stream(Ud.device).cuda_stream
+    _lib.check(_lib.lib().hjb_orthogonality(dt, m, n, Ud.data_ptr(), ld, ctypes.byref(out), st))
+    return float(out.value)

@@ -310,6 +310,27 @@ def test_extract_eigen_gpu(pkg, rng):
         pkg.extract_eigen(Z, J)
 
 
+def test_orthogonality_metric_gpu(pkg, torch, rng):
+    """hjb_orthogonality vs the reference's host formula (solve.py:108-110):
+    ragged/odd shapes, complex, device input, and > 4096 block pairs (two
+    chunks of Gram launches)."""
+    def ref(U):
+        return float(np.abs(U.conj().T @ U - np.eye(U.shape[1])).max())
+
+    cases = [(77, 70, False), (130, 200, True), (64, 64, False), (1, 3, True), (5800, 5800, False)]
+    for m, n, cx in cases:
+        A = rng.standard_normal((m, n)) + (1j * rng.standard_normal((m, n)) if cx else 0)
+        Q = np.linalg.qr(A)[0] if m >= n else A / np.linalg.norm(A, axis=0)
+        U = np.asfortranarray(Q + 1e-7 * rng.standard_normal(Q.shape))
+        for X in (U, A):
+            want = ref(X)
+            got = pkg.orthogonality(X)
+            assert abs(got - want) <= 1e-12 * max(1.0, want) + 64 * m * EPS, (m, n, cx, got, want)
+    Ud = dev_colmajor(torch, U)
+    assert abs(pkg.orthogonality(Ud) - ref(U)) <= 64 * 5800 * EPS
+    assert pkg.orthogonality(np.zeros((5, 0))) == 0.0
+
+
 def test_zero_column_raises_definiteness(pkg, rng):
     G = random_full_rank(rng, 16, 16, False)
     G[:, 3] = 0.0

@@ -10,7 +10,8 @@ checks that need no CPU oracle (SURVEY.md 8(d) "cfg5 oracle"):
 * residual max_i ||H u_i - lam_i u_i|| / (||H|| ||u_i||) over 256 sampled
   columns, H u = G0 (J (G0^H u)) formed on the GPU, ||H|| = max |lam|;
 * J-orthogonality loss off(G_out) = max_{i != j} |g_i^H g_j| / (||g_i|| ||g_j||)
-  for the sampled columns against all columns;
+  for the sampled columns against all columns, and the reference's
+  max |U^H U - I| over all columns (hjb_orthogonality);
 * cfg4: eigenvalues against the prescribed spectrum, bound 64 n eps kappa(G_s)
   with kappa from the scaled Gram (--kappa, GPU eigvalsh).
 
@@ -104,6 +105,11 @@ def main():
     C[torch.arange(len(idx), device=dev), idx] = 0
     out["orth_loss_sampled"] = float(C.max())
     out["orth_bound"] = 64 * n * EPS
+    # the reference's metric over ALL columns (solve.py:108-110) on the GPU
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out["orthogonality_full"] = P.orthogonality(Un)
+    out["orthogonality_full_s"] = time.perf_counter() - t0
     del C, Un, HU, R, U
     if lam_ref is not None:
         ls = np.sort(lam.cpu().numpy())
