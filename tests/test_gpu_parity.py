@@ -374,3 +374,9 @@ def test_cfg4_proxy_solve_hermitian_known_spectrum(pkg):
     assert np.all(np.abs(lam - w.lam) <= 64 * w.n * EPS * kappa * np.abs(w.lam))
     assert metrics["orthogonality"] <= 64 * w.n * EPS
     assert metrics["residual"] <= 64 * w.n * EPS
+    # the GPU metrics agree with the reference's host formulas (solve.py:108-114)
+    U = res.eigenvectors
+    orth_h = float(np.abs(U.conj().T @ U - np.eye(U.shape[1])).max())
+    res_h = float(np.linalg.norm(w.H @ U - U * res.eigenvalues) / np.linalg.norm(w.H))
+    assert abs(metrics["orthogonality"] - orth_h) <= 4 * w.n * EPS
+    assert abs(metrics["residual"] - res_h) <= 1e-6 * res_h + 4 * w.n * EPS
