@@ -88,3 +88,20 @@ def test_uniform_partition_matches_reference_rule():
 def test_generate_sweep_schedule_surface():
     lay = P.generate_sweep_schedule("rr", 3, 1)
     assert len(lay) == 5 and lay[0] == [(1, 6), (2, 5), (3, 4)]
+
+
+def test_orthogonality_argument_validation():
+    """hjb_orthogonality rejects bad arguments before touching a device, and an
+    empty U has orthogonality 0 (solve.py:108-110 returns 0.0 for U.size == 0)."""
+    import ctypes
+
+    L = _lib.lib()
+    out = ctypes.c_double(-1.0)
+    dummy = ctypes.c_void_p(16)  # never dereferenced on these paths
+    assert L.hjb_orthogonality(_lib.HJB_F64, 4, 4, None, 4, ctypes.byref(out), None) == _lib.HJB_EINVAL
+    assert L.hjb_orthogonality(_lib.HJB_F64, 4, 4, dummy, 3, ctypes.byref(out), None) == _lib.HJB_EINVAL
+    assert L.hjb_orthogonality(_lib.HJB_F64, 5, 4, dummy, 5, ctypes.byref(out), None) == _lib.HJB_EINVAL
+    with pytest.raises(ValueError):
+        _lib.check(_lib.HJB_EINVAL)
+    assert L.hjb_orthogonality(_lib.HJB_C128, 4, 0, dummy, 4, ctypes.byref(out), None) == _lib.HJB_OK
+    assert out.value == 0.0
