@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -121,8 +122,13 @@ Partition uniform_partition(int64_t n, int nbl) {  // blocking.py:63-68
 int gram_splits(int count, int tiles, int64_t m, int kc, int64_t *ksplit) {
   const int64_t chunks = (m + kc - 1) / kc;
   const int64_t per = int64_t(count) * tiles * tiles;
+  static const int smax = [] {  // tuning override (experiments only)
+    const char *e = std::getenv("HJB_GRAM_SPLITS_MAX");
+    const int v = e ? std::atoi(e) : 16;
+    return (v >= 1 && v <= 16) ? v : 16;
+  }();
   int s = 1;
-  while (s < 16 && per * (2 * s) <= 2 * 148 + per / 2 && 2 * s <= chunks) s *= 2;
+  while (2 * s <= smax && per * (2 * s) <= 2 * 148 + per / 2 && 2 * s <= chunks) s *= 2;
   const int64_t cps = (chunks + s - 1) / s;  // chunks per split
   *ksplit = cps * kc;
   return s;
