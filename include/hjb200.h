@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define HJB_ABI_VERSION 1
+#define HJB_ABI_VERSION 2
 
 typedef enum {
   HJB_OK = 0,
@@ -55,10 +55,18 @@ typedef struct {
   void *stream;           /* cudaStream_t to run on; NULL = library stream */
   void *comm;             /* hjb_comm from hjb_comm_init, or NULL for one GPU */
   int32_t flags;          /* HJB_FLAG_* */
+  int32_t first_sweep;    /* resume: G_in is the state after sweep first_sweep-1
+                             (<= 1: a fresh solve); the ring layout of that sweep
+                             is replayed (strategies.py:58-136) */
+  int32_t sweep_count;    /* outer sweeps to run from first_sweep (0: until
+                             convergence or max_sweeps); converged = 1 when the
+                             last one applied no rotation (parallel.py:242-244) */
 } hjb_problem;
 
 #define HJB_FLAG_PHASE_TIMES 1   /* record per-phase device times (adds events) */
-#define HJB_FLAG_NO_GRAPH    2   /* launch kernels directly instead of CUDA graphs */
+#define HJB_FLAG_GATHER_ROOT 4   /* multi-GPU: only rank 0 receives the whole G_out
+                                    (other ranks keep the blocks they hold);
+                                    default: every rank receives it */
 
 typedef struct {
   int32_t sweeps;           /* DiagInfo.sweeps (rotations.py:111) */
@@ -157,6 +165,19 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
               const int8_t *signs_dev, double orth_tol, double quad_tol, int32_t max_sweeps,
               void *W, int64_t *stats, void *R_out, int32_t cluster, void *stream);
 
+/*
+ * The pivot kernel's 2x2 rotation (rot_coef, the restatement of
+ * _kernels.py:53-81) on a batch of 2x2 Gram pivots [[a_rr, a_rs],
+ * [conj(a_rs), a_ss]] with signs (j_rr, j_ss): replaces
+ * compute_plane_rotation (rotations.py:128-155).  Host arrays (a_rs is
+ * float64 or complex128 per dtype); out: double [count][8] = (code, cs, sn,
+ * t, eta, phase_re, phase_im, hyp); code 1 rotation, 0 identity (a_rs == 0),
+ * -1 not positive definite (-> PivotDefinitenessError).  Runs on the
+ * current CUDA device.
+ */
+int hjb_plane_rotations(int32_t dtype, int32_t count, const double *a_rr, const double *a_ss,
+                        const void *a_rs, const int8_t *j_rr, const int8_t *j_ss, double *out);
+
 /* Leading dimension of W / R_out used by hjb_pivot for a given bmax. */
 int hjb_pivot_ld(int32_t bmax);
 /* Debug: record per-CTA phase clocks of later hjb_pivot calls into a device
@@ -195,6 +216,15 @@ int hjb_update(int32_t dtype, int64_t m, void *G, int64_t ldg, const int32_t *it
  */
 int hjb_exchange_plan(int32_t strategy, int32_t p, int32_t world, int32_t rank, int32_t sweeps,
                       int32_t max_xfers, int32_t *out, int32_t *counts);
+
+/*
+ * Final block ownership of the multi-GPU ring (host-only): owner[b] = GPU
+ * holding 0-based block b after `sweeps` complete sweeps -- the layout
+ * parallel_jacobi reassembles G_out from (parallel.py:299-301).  The ring
+ * layout repeats every 2 sweeps (strategies.py:69-72), so odd and even sweep
+ * counts give different owners.  owner: int32 [2p].
+ */
+int hjb_block_owners(int32_t strategy, int32_t p, int32_t world, int32_t sweeps, int32_t *owner);
 
 /* 128-byte NCCL unique id for rank 0 to broadcast (e.g. via torch.distributed). */
 int hjb_comm_unique_id(char out[128]);

@@ -19,7 +19,8 @@ from .errors import (
 from .factorization import (FactoredForm, accept_external_factor, factorize_hermitian_indefinite,
                             order_by_inertia, scaled_condition)
 from .parallel import SolverConfig, parallel_jacobi
-from .rotations import DiagInfo, Tolerances, extract_eigen, orthogonality
+from .rotations import (HYPERBOLIC, IDENTITY, TRIGONOMETRIC, DiagInfo, PlaneRotation, Tolerances,
+                        compute_plane_rotation, extract_eigen, orthogonality)
 from .solve import SolveOptions, run_solver, solve_hermitian
 from .strategies import MODULUS, ROUND_ROBIN, generate_sweep_schedule, normalize_strategy, steps_per_sweep
 
@@ -33,4 +34,5 @@ __all__ = [
     "normalize_strategy", "num_blocks", "parallel_jacobi", "steps_per_sweep", "uniform_partition",
     "FactoredForm", "accept_external_factor", "factorize_hermitian_indefinite", "order_by_inertia",
     "scaled_condition", "SolveOptions", "run_solver", "solve_hermitian",
+    "PlaneRotation", "compute_plane_rotation", "TRIGONOMETRIC", "HYPERBOLIC", "IDENTITY",
 ]

@@ -21,7 +21,7 @@ HJB_F64, HJB_C128 = 0, 1
 HJB_MODULUS, HJB_ROUND_ROBIN = 0, 1
 HJB_HOST, HJB_DEVICE = 0, 1
 HJB_FLAG_PHASE_TIMES = 1
-HJB_FLAG_NO_GRAPH = 2
+HJB_FLAG_GATHER_ROOT = 4
 ST_N = 8
 
 
@@ -34,6 +34,7 @@ class Problem(C.Structure):
         ("orth_tol", C.c_double), ("quad_tol", C.c_double),
         ("max_sweeps", C.c_int32), ("device", C.c_int32),
         ("stream", C.c_void_p), ("comm", C.c_void_p), ("flags", C.c_int32),
+        ("first_sweep", C.c_int32), ("sweep_count", C.c_int32),
     ]
 
 
@@ -72,6 +73,8 @@ SIGNATURES = {
                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "hjb_pivot_ld": (C.c_int, [C.c_int32]),
+    "hjb_plane_rotations": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]),
     "hjb_pivot_set_profile": (C.c_int, [C.c_void_p]),
     "hjb_tune": (C.c_int, [C.c_int32, C.c_int32]),
     "hjb_pivot_occupancy": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
@@ -81,6 +84,7 @@ SIGNATURES = {
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hjb_exchange_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_void_p, C.c_void_p]),
+    "hjb_block_owners": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "hjb_comm_unique_id": (C.c_int, [C.c_void_p]),
     "hjb_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     "hjb_comm_destroy": (C.c_int, [C.c_void_p]),
@@ -105,7 +109,7 @@ def lib():
                     fn = getattr(L, name)
                     fn.restype = res
                     fn.argtypes = args
-                if L.hjb_version() != 1:
+                if L.hjb_version() != 2:
                     raise RuntimeError("libhjb200.so ABI version mismatch")
                 # tuning overrides for experiments (0 = the library's heuristic)
                 nt, cl = int(os.environ.get("HJB_PIVOT_THREADS", 0)), int(os.environ.get("HJB_PIVOT_CLUSTER", 0))

@@ -102,6 +102,18 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Per-device "function attributes already set" flag: cudaFuncSetAttribute
+// applies to the current device only, so a per-process flag would skip the
+// attribute on the second device a process uses.
+struct DeviceFlags {
+  bool set[64] = {};
+  bool *here() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return nullptr;
+    return &set[d];
+  }
+};
+
 // one pair-step work item: block column offsets/widths (nj == 0: single block)
 struct Item {
   int32_t oi, ni, oj, nj;

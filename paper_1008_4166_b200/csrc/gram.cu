@@ -253,15 +253,17 @@ static cudaError_t launch_gram_cl(const GramArgs &a, cudaStream_t st) {
   static_assert(Cfg::TILE * Cfg::TILE * sizeof(T) + 2 * Cfg::TILE * sizeof(double) <= Cfg::SMEM,
                 "partial tile fits the staging buffers");
   auto k = gram_kernel<T, WM, KC, STAGES, VEC, CL>;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr_flags;
+  bool *attr = attr_flags.here();
+  if (!attr) return cudaErrorInvalidDevice;
+  if (!*attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));
     if (e != cudaSuccess) return e;
     if (CL > 8) {
       e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
-    attr = true;
+    *attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.tiles * a.tiles * CL, 1, a.count);

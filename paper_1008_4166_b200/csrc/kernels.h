@@ -16,11 +16,8 @@ struct GramArgs {
   int tiles;        // tiles per dimension (set by launch_gram)
   int splits;       // split-K factor
   int64_t ksplit;   // rows per split (multiple of the K chunk)
-  void *Apart;      // [count][splits][bmax*bmax] partials (splits > 1)
-  double *Dpart;    // [count][splits][2*bmax]
   void *A;          // [count][bmax*bmax] final Gram, column-major ld bmax
   double *D;        // [count][2*bmax] final column norms^2
-  unsigned *tickets;  // [count][tiles*tiles], zero-initialised
 };
 cudaError_t launch_gram(bool cx, GramArgs a, cudaStream_t st);
 int gram_tile(int bmax);
@@ -56,6 +53,9 @@ size_t pivot_check_elems(int nmax);
 // the (cluster, threads) launch_pivot picks when not told (honours hjb_tune)
 int pivot_choose_cluster(bool cx, int nmax, int count);
 int pivot_choose_threads(bool cx, int nmax, int c);  // Gram-check scratch elements per item
+
+cudaError_t launch_plane_rotations(bool cx, int count, const double *arr, const double *ass, const void *ars,
+                                   const int8_t *same, double *out, cudaStream_t st);
 
 struct UpdateArgs {
   void *G;

@@ -260,6 +260,50 @@ __device__ __forceinline__ void rot_fold<cplx>(cplx &xr, cplx &xs, const RotCoef
   xs = ns;
 }
 
+// compute_plane_rotation (rotations.py:128-155) for a batch of 2x2 Gram
+// pivots [[a_rr, a_rs], [conj(a_rs), a_ss]] through the pivot kernel's own
+// rot_coef (no skip threshold: only a_rs == 0 is the identity).  out[k] =
+// (code, cs, sn, t, eta, phase_re, phase_im, hyp); code 0 identity, 1
+// rotation, -1 not positive definite (rotations.py:134-135, 147-148).
+template <typename T>
+__global__ void plane_rotation_kernel(int count, const double *arr, const double *ass, const T *ars,
+                                      const int8_t *same, double *out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const double dr = arr[k], ds = ass[k];
+  const T a = ars[k];
+  double *o = out + int64_t(k) * 8;
+  if (!(dr > 0.0) || !(ds > 0.0)) {
+    o[0] = -1.0;
+    return;
+  }
+  const RotCoef<T> p = rot_coef<T>(a, dr, ds, same[k] != 0, 0.0);
+  const double q = abs2(a);
+  const double ri = q > 0.0 ? rsqrt(q) : 0.0;
+  const double sa = re(a) >= 0.0 ? 1.0 : -1.0;
+  T ph = phase_mul(a, sa * ri);
+  o[0] = p.code;
+  o[1] = p.code == 1 ? p.cs : 1.0;
+  o[2] = p.code == 1 ? p.hs * p.hyp : 0.0;  // sn (hs = hyp * sn)
+  o[3] = p.code == 1 ? p.num / p.den : 0.0;
+  o[4] = p.code == 1 ? p.eta : 0.0;
+  o[5] = p.code == 1 ? re(ph) : 1.0;
+  if constexpr (S<T>::cx) o[6] = p.code == 1 ? ph.y : 0.0;
+  else o[6] = 0.0;
+  o[7] = p.hyp;
+}
+
+cudaError_t launch_plane_rotations(bool cx, int count, const double *arr, const double *ass, const void *ars,
+                                   const int8_t *same, double *out, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int nb = (count + 127) / 128;
+  if (cx)
+    plane_rotation_kernel<cplx><<<nb, 128, 0, st>>>(count, arr, ass, static_cast<const cplx *>(ars), same, out);
+  else
+    plane_rotation_kernel<double><<<nb, 128, 0, st>>>(count, arr, ass, static_cast<const double *>(ars), same, out);
+  return cudaGetLastError();
+}
+
 template <typename T, int NMAX, int C, int NT>
 __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   using Cfg = PivCfg<T, NMAX, C, NT>;
@@ -1395,15 +1439,17 @@ template <typename T, int NMAX, int C, int NT>
 static cudaError_t launch_pivot_t(const PivotArgs &a, cudaStream_t st) {
   using Cfg = PivCfg<T, NMAX, C, NT>;
   auto k = pivot_kernel<T, NMAX, C, NT>;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr_flags;
+  bool *attr = attr_flags.here();
+  if (!attr) return cudaErrorInvalidDevice;
+  if (!*attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));
     if (e != cudaSuccess) return e;
     if (C > 8) {
       e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
-    attr = true;
+    *attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.count * C);

@@ -110,4 +110,16 @@ void step_transfers(const std::vector<StepPlan> &plans, int p, int world, int ra
   }
 }
 
+std::vector<int> final_block_owners(int strategy, int p, int world, int sweeps) {
+  RingSchedule rs(strategy, p);
+  for (int sw = 1; sw <= sweeps; ++sw)
+    for (int s = 0; s < rs.steps_per_sweep(); ++s) rs.advance(sw);
+  std::vector<int> owner(2 * p, -1);
+  for (int q = 0; q < p; ++q) {
+    owner[rs.i_blk(q) - 1] = gpu_of_worker(p, world, q);
+    owner[rs.j_blk(q) - 1] = gpu_of_worker(p, world, q);
+  }
+  return owner;
+}
+
 }  // namespace hjb

@@ -50,4 +50,9 @@ struct Xfer {
 // (parallel.py:212-221); only partners on another GPU need a transfer.
 void step_transfers(const std::vector<StepPlan> &plans, int p, int world, int rank, std::vector<Xfer> &out);
 
+// GPU holding each block (0-based) after `sweeps` whole sweeps of the ring
+// (the layout the reference reassembles from, parallel.py:299-301).  The
+// layout has period 2 sweeps, so odd and even sweep counts differ.
+std::vector<int> final_block_owners(int strategy, int p, int world, int sweeps);
+
 }  // namespace hjb

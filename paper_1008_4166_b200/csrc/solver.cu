@@ -82,7 +82,7 @@ struct HBuf {
 };
 
 struct Workspace {
-  DBuf G, items, A, Apart, D, Dpart, tickets, W, U, Gc, stats, signs, red, lam, flag;
+  DBuf G, items, A, D, W, U, Gc, stats, signs, red, lam, flag;
   HBuf stats_h, red_h;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> events;
@@ -97,6 +97,8 @@ struct Comm {
 };
 
 size_t esz(int dtype) { return dtype == HJB_C128 ? 16 : 8; }
+
+constexpr int RED_N = 9;  // int64 DiagInfo counters all-reduced at the end of a multi-GPU solve
 
 struct Partition {
   std::vector<int> off, width;  // per block (0-based block index)
@@ -165,11 +167,8 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   g.bmax = c.bmax;
   g.splits = splits;
   g.ksplit = ksplit;
-  g.Apart = c.ws->Apart.p;
-  g.Dpart = static_cast<double *>(c.ws->Dpart.p);
   g.A = c.ws->A.p;
   g.D = static_cast<double *>(c.ws->D.p);
-  g.tickets = static_cast<unsigned *>(c.ws->tickets.p);
   if (ev) CK(cudaEventRecord(ev[0], c.st));
   CK(launch_gram(c.cx, g, c.st));
   if (ev) CK(cudaEventRecord(ev[1], c.st));
@@ -212,21 +211,9 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
 
 int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_count, int64_t m) {
   const size_t w = cx ? 16 : 8;
-  const int tile = gram_tile(bmax);
-  const int tiles = (bmax + tile - 1) / tile;
-  int64_t ks = 0;
-  int max_splits = 1;
-  for (int cnt = 1; cnt <= max_count; cnt = cnt < max_count ? std::min(max_count, cnt * 2) : cnt + 1)
-    max_splits = std::max(max_splits, gram_splits(cnt, tiles, m, gram_kc(cx), &ks));
+  (void)m;
   CK(ws.A.reserve(size_t(max_count) * bmax * bmax * w));
-  CK(ws.Apart.reserve(size_t(max_count) * max_splits * bmax * bmax * w));
   CK(ws.D.reserve(size_t(max_count) * 2 * bmax * 8));
-  CK(ws.Dpart.reserve(size_t(max_count) * max_splits * 2 * bmax * 8));
-  const size_t tk = size_t(max_count) * tiles * tiles * sizeof(unsigned);
-  if (ws.tickets.n < tk) {
-    CK(ws.tickets.reserve(tk));
-    CK(cudaMemset(ws.tickets.p, 0, ws.tickets.n));
-  }
   CK(ws.W.reserve(size_t(max_count) * nmax * nmax * w));
   CK(ws.U.reserve(size_t(max_count) * (nmax / 2) * (nmax / 2 + 1) * w));  // pivot factor U (L2 scratch)
   CK(ws.Gc.reserve(size_t(max_count) * pivot_check_elems(nmax) * w));    // final-sweep Gram check
@@ -302,6 +289,19 @@ int hjb_exchange_plan(int32_t strategy, int32_t p, int32_t world, int32_t rank, 
           o[2] = xf[t].send ? 1 : 0;
         }
       }
+  } catch (const std::exception &e) {
+    return fail(HJB_EINVAL, e.what());
+  }
+  return HJB_OK;
+}
+
+int hjb_block_owners(int32_t strategy, int32_t p, int32_t world, int32_t sweeps, int32_t *owner) {
+  if (p < 1 || world < 1 || p < world || sweeps < 0 || !owner ||
+      (strategy != HJB_MODULUS && strategy != HJB_ROUND_ROBIN))
+    return fail(HJB_EINVAL, "hjb_block_owners: invalid argument");
+  try {
+    const std::vector<int> o = final_block_owners(strategy, p, world, sweeps);
+    for (int b = 0; b < 2 * p; ++b) owner[b] = o[b];
   } catch (const std::exception &e) {
     return fail(HJB_EINVAL, e.what());
   }
@@ -421,18 +421,31 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   CK(ws.signs.reserve(n));
   CK(cudaMemcpyAsync(ws.signs.p, pr->signs, n, cudaMemcpyHostToDevice, st));
 
+  // ---- sweep range: [s0, s1] (a resumed solve starts at sweep s0 from the
+  // state G_in had after sweep s0 - 1; the ring layout is data-independent) ----
+  const int s0 = std::max(1, pr->first_sweep);
+  if (s0 > pr->max_sweeps) return fail(HJB_EINVAL, "first_sweep > max_sweeps");
+  if (pr->sweep_count < 0) return fail(HJB_EINVAL, "sweep_count must be >= 0");
+  const int s1 = pr->sweep_count > 0 ? std::min(pr->max_sweeps, s0 + pr->sweep_count - 1) : pr->max_sweeps;
+  const int nsw = s1 - s0 + 1;
+
   // ---- schedule -> per-sweep item tables of this GPU's workers ----
   RingSchedule ring(pr->strategy, P);
   const int steps = ring.steps_per_sweep();
-  auto gpu_of = [&](int q) { return gpu_of_worker(P, world, q); };
-  const int q_lo = workers_lo(P, world, grank), q_hi = workers_lo(P, world, grank + 1), nloc = q_hi - q_lo;
-  // layouts for max_sweeps sweeps: [sweep][1 + steps][nloc or 2*nloc]
-  const int per_sweep_items = 2 * nloc + steps * nloc;
-  std::vector<Item> items(size_t(pr->max_sweeps) * per_sweep_items);
-  std::vector<std::vector<Xfer>> xfers(size_t(pr->max_sweeps) * steps);
   try {
-    for (int sw = 1; sw <= pr->max_sweeps; ++sw) {
-      Item *base = items.data() + size_t(sw - 1) * per_sweep_items;
+    for (int sw = 1; sw < s0; ++sw)
+      for (int s = 0; s < steps; ++s) ring.advance(sw);
+  } catch (const std::exception &e) {
+    return fail(HJB_EINVAL, e.what());
+  }
+  const int q_lo = workers_lo(P, world, grank), q_hi = workers_lo(P, world, grank + 1), nloc = q_hi - q_lo;
+  // layouts for sweeps s0..s1: [sweep - s0][1 + steps][nloc or 2*nloc]
+  const int per_sweep_items = 2 * nloc + steps * nloc;
+  std::vector<Item> items(size_t(nsw) * per_sweep_items);
+  std::vector<std::vector<Xfer>> xfers(size_t(nsw) * steps);
+  try {
+    for (int sw = s0; sw <= s1; ++sw) {
+      Item *base = items.data() + size_t(sw - s0) * per_sweep_items;
       for (int q = q_lo; q < q_hi; ++q) {  // pre-pass: the two blocks each worker holds
         const int bi = ring.i_blk(q) - 1, bj = ring.j_blk(q) - 1;
         base[2 * (q - q_lo) + 0] = Item{part.off[bi], part.width[bi], 0, 0};
@@ -445,7 +458,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
           row[q - q_lo] = Item{part.off[bi], part.width[bi], part.off[bj], part.width[bj]};
         }
         std::vector<StepPlan> pl = ring.advance(sw);
-        step_transfers(pl, P, world, grank, xfers[size_t(sw - 1) * steps + s]);
+        step_transfers(pl, P, world, grank, xfers[size_t(sw - s0) * steps + s]);
       }
     }
   } catch (const std::exception &e) {
@@ -458,8 +471,8 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   const size_t stats_per_sweep = size_t(per_sweep_items) * ST_N;
   CK(ws.stats.reserve(2 * stats_per_sweep * sizeof(int64_t)));
   CK(ws.stats_h.reserve(stats_per_sweep * sizeof(int64_t)));
-  CK(ws.red.reserve(4 * sizeof(int64_t)));
-  CK(ws.red_h.reserve(4 * sizeof(int64_t)));
+  CK(ws.red.reserve((RED_N + 1) * sizeof(int64_t)));
+  CK(ws.red_h.reserve((RED_N + 1) * sizeof(int64_t)));
 
   const bool phase_times = pr->flags & HJB_FLAG_PHASE_TIMES;
   const int nev = phase_times ? 4 * (1 + steps) + 2 * steps : 0;
@@ -489,8 +502,8 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   std::vector<int64_t> hstats(stats_per_sweep);
   double tg = 0, tp = 0, tu = 0, tx = 0;
 
-  for (int sw = 1; sw <= pr->max_sweeps; ++sw) {
-    const Item *it_d = static_cast<const Item *>(ws.items.p) + size_t(sw - 1) * per_sweep_items;
+  for (int sw = s0; sw <= s1; ++sw) {
+    const Item *it_d = static_cast<const Item *>(ws.items.p) + size_t(sw - s0) * per_sweep_items;
     int64_t *stats_d = static_cast<int64_t *>(ws.stats.p) + size_t((sw - 1) & 1) * stats_per_sweep;
     cudaEvent_t *ev = phase_times ? &ws.events[2] : nullptr;
     if (int rc = run_phase(ctx, it_d, 2 * nloc, stats_d, nullptr, ev)) return rc;
@@ -499,7 +512,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
       if (int rc = run_phase(ctx, it_d + 2 * nloc + s * nloc, nloc,
                              stats_d + size_t(2 * nloc + s * nloc) * ST_N, nullptr, evs))
         return rc;
-      const auto &xf = xfers[size_t(sw - 1) * steps + s];
+      const auto &xf = xfers[size_t(sw - s0) * steps + s];
       if (!xf.empty()) {
         if (phase_times) CK(cudaEventRecord(ws.events[2 + 4 * (1 + steps) + 2 * s], st));
         NK(ncclGroupStart());
@@ -526,7 +539,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
     for (int t = 0; t < per_sweep_items; ++t) {
       const int64_t *sv = hstats.data() + size_t(t) * ST_N;
       const bool pre = t < 2 * nloc;
-      const Item &itm = items[size_t(sw - 1) * per_sweep_items + t];
+      const Item &itm = items[size_t(sw - s0) * per_sweep_items + t];
       const int64_t Nq = itm.ni + itm.nj;
       res->inner_sweeps += sv[ST_SWEEPS];
       res->inner_pair_visits += sv[ST_SWEEPS] * (Nq * (Nq - 1) / 2);
@@ -566,7 +579,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
         CK(cudaEventElapsedTime(&ms, e[2], e[3])); tu += ms;
       }
       for (int s = 0; s < steps; ++s)
-        if (!xfers[size_t(sw - 1) * steps + s].empty()) {
+        if (!xfers[size_t(sw - s0) * steps + s].empty()) {
           CK(cudaEventElapsedTime(&ms, ws.events[2 + 4 * (1 + steps) + 2 * s],
                                   ws.events[2 + 4 * (1 + steps) + 2 * s + 1]));
           tx += ms;
@@ -597,17 +610,48 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
     }
   }
 
-  // ---- gather: every block from the GPU whose worker holds it ----
+  // ---- DiagInfo over all GPUs (parallel.py:302-308: sums over workers,
+  // max of max |t|) ----
   if (comm) {
-    std::vector<int> owner(nbl, 0);
-    for (int q = 0; q < P; ++q) {
-      owner[ring.i_blk(q) - 1] = gpu_of(q);
-      owner[ring.j_blk(q) - 1] = gpu_of(q);
+    int64_t *rh = static_cast<int64_t *>(ws.red_h.p);
+    const int64_t mine[RED_N] = {res->rotations,       res->big_rotations,  res->pairs_visited,
+                                 res->pairs_updated,   res->prepass_visited, res->prepass_updated,
+                                 res->fallbacks,       res->inner_sweeps,   res->inner_pair_visits};
+    std::memcpy(rh, mine, sizeof(mine));
+    CK(cudaMemcpyAsync(ws.red.p, rh, sizeof(mine), cudaMemcpyHostToDevice, st));
+    NK(ncclAllReduce(ws.red.p, ws.red.p, RED_N, ncclInt64, ncclSum, comm->nccl, st));
+    double *mt = reinterpret_cast<double *>(static_cast<int64_t *>(ws.red.p) + RED_N);
+    CK(cudaMemcpyAsync(mt, &res->max_abs_t, sizeof(double), cudaMemcpyHostToDevice, st));
+    NK(ncclAllReduce(mt, mt, 1, ncclFloat64, ncclMax, comm->nccl, st));
+    CK(cudaMemcpyAsync(rh, ws.red.p, RED_N * sizeof(int64_t) + sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int64_t *dst[RED_N] = {&res->rotations,       &res->big_rotations,   &res->pairs_visited,
+                           &res->pairs_updated,   &res->prepass_visited, &res->prepass_updated,
+                           &res->fallbacks,       &res->inner_sweeps,    &res->inner_pair_visits};
+    for (int k = 0; k < RED_N; ++k) *dst[k] = rh[k];
+    std::memcpy(&res->max_abs_t, rh + RED_N, sizeof(double));
+  }
+
+  // ---- gather: every block from the GPU whose worker holds it after the
+  // sweeps actually run (parallel.py:299-301) ----
+  if (comm) {
+    std::vector<int> owner;
+    try {
+      owner = final_block_owners(pr->strategy, P, world, res->sweeps);
+    } catch (const std::exception &e) {
+      return fail(HJB_EINVAL, e.what());
     }
+    const bool to_root = pr->flags & HJB_FLAG_GATHER_ROOT;
     NK(ncclGroupStart());
     for (int b = 0; b < nbl; ++b) {
       char *ptr = static_cast<char *>(Gd) + size_t(part.off[b]) * ld * w;
-      NK(ncclBroadcast(ptr, ptr, size_t(part.width[b]) * ld * w, ncclChar, owner[b], comm->nccl, st));
+      const size_t bytes = size_t(part.width[b]) * ld * w;
+      if (!to_root) {
+        NK(ncclBroadcast(ptr, ptr, bytes, ncclChar, owner[b], comm->nccl, st));
+      } else if (owner[b] != 0) {  // rank 0 receives every block it does not hold
+        if (grank == owner[b]) NK(ncclSend(ptr, bytes, ncclChar, 0, comm->nccl, st));
+        if (grank == 0) NK(ncclRecv(ptr, bytes, ncclChar, owner[b], comm->nccl, st));
+      }
     }
     NK(ncclGroupEnd());
   }
@@ -628,6 +672,36 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
 }
 
 // ---------------------------------------------------------------- kernel-level entry points
+
+int hjb_plane_rotations(int32_t dtype, int32_t count, const double *a_rr, const double *a_ss, const void *a_rs,
+                        const int8_t *j_rr, const int8_t *j_ss, double *out) {
+  if (count < 0 || (count > 0 && (!a_rr || !a_ss || !a_rs || !j_rr || !j_ss || !out)))
+    return fail(HJB_EINVAL, "hjb_plane_rotations: bad arguments");
+  if (count == 0) return HJB_OK;
+  const bool cx = dtype == HJB_C128;
+  const size_t w = cx ? 16 : 8;
+  std::vector<int8_t> same(count);
+  for (int k = 0; k < count; ++k) same[k] = j_rr[k] == j_ss[k];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  char *buf = nullptr;
+  const size_t bytes = size_t(count) * (8 + 8 + w + 1 + 64) + 64;
+  CK(cudaMalloc(&buf, bytes));
+  double *darr = reinterpret_cast<double *>(buf);
+  double *dass = darr + count;
+  char *dars = reinterpret_cast<char *>(dass + count);
+  double *dout = reinterpret_cast<double *>(dars + size_t(count) * w);
+  int8_t *dsame = reinterpret_cast<int8_t *>(dout + size_t(count) * 8);
+  cudaError_t e = cudaMemcpy(darr, a_rr, count * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dass, a_ss, count * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dars, a_rs, count * w, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dsame, same.data(), count, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_plane_rotations(cx, count, darr, dass, dars, dsame, dout, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, size_t(count) * 64, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  CK(e);
+  return HJB_OK;
+}
 
 static int upload_items(Workspace &ws, const int32_t *items_host, int count, cudaStream_t st) {
   CK(ws.items.reserve(size_t(count) * sizeof(Item)));
@@ -656,11 +730,8 @@ int hjb_gram(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_t
   g.count = count;
   g.bmax = bmax;
   g.splits = gram_splits(count, tiles, m, gram_kc(cx), &g.ksplit);
-  g.Apart = ws.Apart.p;
-  g.Dpart = static_cast<double *>(ws.Dpart.p);
   g.A = A;
   g.D = D;
-  g.tickets = static_cast<unsigned *>(ws.tickets.p);
   CK(launch_gram(cx, g, st));
   CK(cudaStreamSynchronize(st));
   return HJB_OK;
@@ -793,11 +864,8 @@ int hjb_orthogonality(int32_t dtype, int64_t m, int64_t n, const void *U, int64_
     g.count = count;
     g.bmax = bw;
     g.splits = gram_splits(count, tiles, m, gram_kc(cx), &g.ksplit);
-    g.Apart = ws.Apart.p;
-    g.Dpart = static_cast<double *>(ws.Dpart.p);
     g.A = ws.A.p;
     g.D = static_cast<double *>(ws.D.p);
-    g.tickets = static_cast<unsigned *>(ws.tickets.p);
     CK(launch_gram(cx, g, st));
     CK(launch_orth_max(cx, items_d, count, bw, ws.A.p, acc, st));
   }

@@ -155,11 +155,13 @@ template <typename T, int NMAX, int MT, int KW, int VEC>
 static cudaError_t launch_update_t(const UpdateArgs &a, cudaStream_t st) {
   using Cfg = UpdCfg<T, NMAX, MT, KW>;
   auto k = update_kernel<T, NMAX, MT, KW, VEC>;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr_flags;
+  bool *attr = attr_flags.here();
+  if (!attr) return cudaErrorInvalidDevice;
+  if (!*attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));
     if (e != cudaSuccess) return e;
-    attr = true;
+    *attr = true;
   }
   dim3 grid(unsigned((a.m + MT - 1) / MT), a.count);
   k<<<grid, Cfg::NT, Cfg::SMEM, st>>>(a);

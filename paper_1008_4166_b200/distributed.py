@@ -42,6 +42,15 @@ def exchange_plan(strategy: str, p: int, world: int, rank: int, sweeps: int = 1)
     return [[(int(b), int(pe), bool(sd)) for b, pe, sd in out[s, :cnt[s]]] for s in range(steps)]
 
 
+def block_owners(strategy: str, p: int, world: int, sweeps: int):
+    """GPU holding each 0-based block after ``sweeps`` sweeps (hjb_block_owners,
+    the map hjb_solve gathers G_out from; parallel.py:299-301)."""
+    from .strategies import strategy_code
+    out = np.zeros(2 * p, np.int32)
+    _lib.check(_lib.lib().hjb_block_owners(strategy_code(strategy), p, world, sweeps, out.ctypes.data))
+    return out
+
+
 class Comm:
     """Handle passed as SolverConfig.comm."""
 

@@ -28,7 +28,12 @@ SUPPORTED_VARIANTS = ("2F",)
 class SolverConfig:
     """Same fields and validation as parallel.py:46-62, plus the B200 knobs
     ``device`` (CUDA ordinal, default current), ``comm`` (multi-GPU handle
-    from ``paper_1008_4166_b200.distributed``) and ``phase_times``."""
+    from ``paper_1008_4166_b200.distributed``), ``phase_times``,
+    ``gather_root`` (multi-GPU: only rank 0 receives G_out) and the
+    checkpoint/resume pair ``first_sweep`` / ``sweep_count`` (G is the state
+    after sweep first_sweep-1; run sweep_count sweeps, 0 = to convergence).
+    The state at a sweep boundary is (G, sweep index): the ring layout is
+    data-independent (strategies.py:58-136) and D is recomputed."""
 
     variant: str
     strategy: str = MODULUS
@@ -39,6 +44,9 @@ class SolverConfig:
     device: int | None = None
     comm: object = None
     phase_times: bool = False
+    gather_root: bool = False
+    first_sweep: int = 1
+    sweep_count: int = 0
 
     def __post_init__(self):
         if self.variant not in VARIANTS:
@@ -48,6 +56,8 @@ class SolverConfig:
             raise ValueError("p must be >= 1")
         if self.inner_n_t < 1:
             raise ValueError("inner_n_t must be >= 1")
+        if self.first_sweep < 1 or self.sweep_count < 0:
+            raise ValueError("first_sweep must be >= 1 and sweep_count >= 0")
 
 
 def _info_from(res: _lib.Result) -> DiagInfo:
@@ -71,7 +81,10 @@ def _problem(cfg: SolverConfig, m, n, ld, cx, mem, gin, gout, signs, device, str
     pr.device = device
     pr.stream = stream
     pr.comm = cfg.comm.handle if cfg.comm is not None else None
-    pr.flags = _lib.HJB_FLAG_PHASE_TIMES if cfg.phase_times else 0
+    pr.flags = (_lib.HJB_FLAG_PHASE_TIMES if cfg.phase_times else 0) | \
+        (_lib.HJB_FLAG_GATHER_ROOT if cfg.gather_root else 0)
+    pr.first_sweep = cfg.first_sweep
+    pr.sweep_count = cfg.sweep_count
     return pr
 
 

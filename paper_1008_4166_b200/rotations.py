@@ -11,9 +11,62 @@ import numpy as np
 
 from . import _device, _lib
 from .core import EigenResult
-from .errors import StructuralError
+from .errors import PivotDefinitenessError, StructuralError
 
 EPS = float(np.finfo(np.float64).eps)
+
+
+TRIGONOMETRIC = "trigonometric"
+HYPERBOLIC = "hyperbolic"
+IDENTITY = "identity"
+
+
+@dataclass(frozen=True)
+class PlaneRotation:
+    """Nontrivial 2x2 part of a J-unitary plane transformation (same fields
+    and ``matrix`` convention as rotations.py:24-53)."""
+
+    kind: str
+    cs: float
+    sn: float
+    phase: complex
+    t: float
+    eta: float = 0.0
+
+    @property
+    def matrix(self):
+        """W_P with [g_r', g_s'] = [g_r, g_s] W_P (rotations.py:42-53)."""
+        if self.kind == IDENTITY:
+            return np.eye(2)
+        sigma = 1.0 if self.kind == HYPERBOLIC else -1.0
+        return np.array([[self.cs * self.phase, self.sn * self.phase], [sigma * self.sn, self.cs]])
+
+
+def compute_plane_rotation(a_rr, a_ss, a_rs, j_rr, j_ss):
+    """compute_plane_rotation (rotations.py:128-155) evaluated by the pivot
+    kernel's own rotation code on the GPU (hjb_plane_rotations): the 2x2
+    parameters the B200 path applies.  Raises PivotDefinitenessError(0, 1)
+    for a pivot that is not positive definite (rotations.py:134-135, 147-148)."""
+    import ctypes
+
+    cx = isinstance(a_rs, complex) or np.iscomplexobj(a_rs)
+    arr = np.array([float(a_rr)])
+    ass = np.array([float(a_ss)])
+    ars = np.array([a_rs], np.complex128 if cx else np.float64)
+    jr = np.array([int(j_rr)], np.int8)
+    js = np.array([int(j_ss)], np.int8)
+    out = np.zeros(8)
+    _lib.check(_lib.lib().hjb_plane_rotations(_lib.HJB_C128 if cx else _lib.HJB_F64, 1, arr.ctypes.data,
+                                              ass.ctypes.data, ars.ctypes.data, jr.ctypes.data,
+                                              js.ctypes.data, out.ctypes.data))
+    code, cs, sn, t, eta, ph_re, ph_im, _ = out
+    if code < 0:
+        raise PivotDefinitenessError(0, 1, "2x2 pivot is not positive definite")
+    if code == 0:
+        return PlaneRotation(IDENTITY, 1.0, 0.0, 1.0, 0.0, 0.0)
+    phase = complex(ph_re, ph_im) if cx else ph_re
+    kind = TRIGONOMETRIC if int(j_rr) == int(j_ss) else HYPERBOLIC
+    return PlaneRotation(kind, float(cs), float(sn), phase, float(t), float(eta))
 
 
 @dataclass(frozen=True)

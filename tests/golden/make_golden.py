@@ -159,6 +159,39 @@ def config_proxies():
         json.dump(meta, f, indent=1)
 
 
+def fullsize():
+    """BASELINE cfg2 (n=2048) and cfg3 (n=4096) at FULL size with the
+    reference itself (2F, round-robin, p = n/(2b) worker threads, orth_tol =
+    n eps), plus the cfg5 sweep-count proxies at n = 4096, b = 128 (SURVEY.md
+    8(d) cfg5 oracle item iii).  Stored per column: lambda = J ||g||^2 and
+    the column sums of G_out; per run: DiagInfo and the wall time.  G_out
+    itself (64-128 MiB) is not stored.  kappa(G_s) (factorization.py:156-168)
+    of the input is stored for the per-eigenvalue bound."""
+    import time
+    from hjacobi.factorization import scaled_condition
+    which = os.environ.get("HJB_FULLSIZE", "cfg2,cfg3,cfg5r_p,cfg5c_p").split(",")
+    runs = {"cfg2": ("cfg2", {}), "cfg3": ("cfg3", {}),
+            "cfg5r_p": ("cfg5r", {"n": 4096, "b": 128}), "cfg5c_p": ("cfg5c", {"n": 4096, "b": 128})}
+    for tag in which:
+        name, kw = runs[tag]
+        w = workloads.make(name, **kw)
+        tol = Tolerances(orth_tol=w.orth_tol)
+        t0 = time.perf_counter()
+        Gout, info = parallel_jacobi(w.G.copy(order="F"), w.J.copy(),
+                                     SolverConfig(variant="2F", strategy="round_robin",
+                                                  p=w.p, tol=tol))
+        wall = time.perf_counter() - t0
+        kappa = np.sqrt(scaled_condition(gram(w.G)))
+        key = f"{name}_n{w.n}_b{w.b}"
+        out = {key + "_lam": w.J * column_norms_squared(Gout),
+               key + "_colsum": Gout.sum(axis=0),
+               key + "_info": np.array([info.sweeps, info.rotations, info.big_rotations,
+                                        info.max_abs_t, int(info.converged), wall, kappa,
+                                        os.cpu_count()], np.float64)}
+        np.savez_compressed(os.path.join(HERE, f"fullsize_{key}.npz"), **out)
+        print(key, info.sweeps, info.rotations, f"{wall:.1f}s", f"kappa {kappa:.3e}", flush=True)
+
+
 def kernels():
     """Pivot-level pins: structured Cholesky and jacobi_diagonalize."""
     out = {}

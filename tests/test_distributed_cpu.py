@@ -74,14 +74,19 @@ def _rank_main(rank, world, port, G, J, p, strategy, max_sweeps, out_q):
         if int(t[0]) == 0:
             converged = True
             break
-    held = [b - 1 for q in range(lo, hi) for b in ring.layout()[q]]
+    # reassemble from the NATIVE final owner map (hjb_block_owners, what
+    # hjb_solve gathers from), checked against this rank's replayed layout
+    owners = PD.block_owners(strategy, p, world, sweeps_done)
+    held = sorted(b - 1 for q in range(lo, hi) for b in ring.layout()[q])
+    assert held == [b for b in range(nbl) if owners[b] == rank], (held, owners)
     out_q.put((rank, {b: blocks[b] for b in held}, sweeps_done, converged))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cplx,strategy,p", [(False, "round_robin", 4), (True, "modulus", 3)])
-def test_two_rank_ring_matches_single_process(cplx, strategy, p):
+@pytest.mark.parametrize("cplx,strategy,p,max_sweeps", [(False, "round_robin", 4, 30), (True, "modulus", 3, 30),
+                                                        (False, "round_robin", 4, 3), (True, "modulus", 4, 2)])
+def test_two_rank_ring_matches_single_process(cplx, strategy, p, max_sweeps):
     import torch.multiprocessing as mp
 
     rng = np.random.default_rng(11)
@@ -89,11 +94,11 @@ def test_two_rank_ring_matches_single_process(cplx, strategy, p):
     G = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0)
     G = np.asfortranarray(G)
     J = np.array([1] * (n - n // 3) + [-1] * (n // 3), np.int8)
-    ref, info = O.parallel_jacobi_2f(G, J, p, strategy)
+    ref, info = O.parallel_jacobi_2f(G, J, p, strategy, sweep_limit=max_sweeps)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, G, J, p, strategy, 30, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, G, J, p, strategy, max_sweeps, q)) for r in range(2)]
     for pr in procs:
         pr.start()
     got = [q.get(timeout=300) for _ in procs]
@@ -125,3 +130,33 @@ def test_exchange_plan_is_symmetric():
                 assert sends == recvs
                 # one block out and one in per GPU boundary
                 assert all(len(plans[r][s]) <= 2 * max(1, p // world) for r in range(world))
+
+
+def _replayed_owners(strategy, p, world, sweeps):
+    ring = O.RingSchedule(strategy, p)
+    for sw in range(1, sweeps + 1):
+        for _ in range(O.steps_per_sweep(strategy, p)):
+            ring.advance(sw)
+    from paper_1008_4166_b200 import distributed as PD
+    own = np.full(2 * p, -1)
+    for q, (i, j) in enumerate(ring.layout()):
+        own[i - 1] = own[j - 1] = PD.gpu_of_worker(p, world, q)
+    return own
+
+
+@pytest.mark.parametrize("strategy", ["round_robin", "modulus"])
+def test_final_owner_map_odd_and_even_sweeps(strategy):
+    """hjb_block_owners == the oracle's ring replayed through exactly the
+    sweeps run (parallel.py:299-301).  Round 1 read the owners after all
+    max_sweeps advances, which is wrong for every odd sweep count: the
+    layout has period 2 sweeps."""
+    from paper_1008_4166_b200 import distributed as PD
+
+    for p, world in ((16, 2), (32, 2), (128, 8), (64, 4), (7, 3)):
+        for sweeps in (0, 1, 2, 14, 15, 17, 30):
+            got = PD.block_owners(strategy, p, world, sweeps)
+            assert np.array_equal(got, _replayed_owners(strategy, p, world, sweeps)), (p, world, sweeps)
+        # the round-1 bug: owners after max_sweeps (30) instead of the 15 run
+        if p >= 16:
+            assert not np.array_equal(PD.block_owners(strategy, p, world, 15),
+                                      PD.block_owners(strategy, p, world, 30))

@@ -380,3 +380,109 @@ def test_cfg4_proxy_solve_hermitian_known_spectrum(pkg):
     res_h = float(np.linalg.norm(w.H @ U - U * res.eigenvalues) / np.linalg.norm(w.H))
     assert abs(metrics["orthogonality"] - orth_h) <= 4 * w.n * EPS
     assert abs(metrics["residual"] - res_h) <= 1e-6 * res_h + 4 * w.n * EPS
+
+
+# --------------------------------------------------------------------- error paths
+
+def test_plane_rotation_contract_gpu(pkg):
+    """The GPU rotation (rot_coef) on the reference's closed-form 2x2 cases
+    (test_rotations.py:41-68) and its contract (J-unitary, annihilating)."""
+    rot = pkg.compute_plane_rotation(4.0, 2.0, 1.0, 1, 1)  # eigenvalues 3 +- sqrt(2)
+    assert rot.kind == pkg.TRIGONOMETRIC
+    A = np.array([[4.0, 1.0], [1.0, 2.0]])
+    B = rot.matrix.conj().T @ A @ rot.matrix
+    assert sorted(np.diag(B).real) == pytest.approx([3 - math.sqrt(2), 3 + math.sqrt(2)], rel=1e-15)
+    rot = pkg.compute_plane_rotation(2.0, 2.0, 1.0, 1, -1)  # t = -2 + sqrt(3)
+    assert rot.kind == pkg.HYPERBOLIC and rot.t == pytest.approx(-2 + math.sqrt(3), rel=1e-15)
+    B = rot.matrix.conj().T @ np.array([[2.0, 1.0], [1.0, 2.0]]) @ rot.matrix
+    assert np.diag(B).real == pytest.approx([math.sqrt(3)] * 2, rel=1e-14)
+    rot = pkg.compute_plane_rotation(5.0, 7.0, 0.0, 1, 1)
+    assert rot.kind == pkg.IDENTITY and rot.cs == 1.0 and rot.sn == 0.0
+    with pytest.raises(pkg.PivotDefinitenessError):
+        pkg.compute_plane_rotation(1.0, 1.0, 2.0, 1, -1)
+    with pytest.raises(pkg.PivotDefinitenessError):
+        pkg.compute_plane_rotation(1.0, 1.0, 1.0, 1, 1)  # |a|^2 >= a_rr a_ss
+    rng = np.random.default_rng(8)
+    for k in range(300):
+        arr, ass = rng.uniform(0.1, 5.0, 2)
+        a = (rng.standard_normal() + (1j * rng.standard_normal() if k % 2 else 0)) * 0.9 * math.sqrt(arr * ass) / 1.5
+        jr, js = (1, 1) if k % 3 == 0 else (1, -1)
+        rot = pkg.compute_plane_rotation(arr, ass, a, jr, js)
+        W = rot.matrix
+        Jp = np.diag([float(jr), float(js)])
+        Ap = np.array([[arr, a], [np.conj(a), ass]])
+        assert np.abs(W.conj().T @ Jp @ W - Jp).max() <= 16 * EPS * max(1.0, np.abs(W).max() ** 2)
+        assert abs((W.conj().T @ Ap @ W)[0, 1]) <= 16 * EPS * np.abs(Ap).max() * max(1.0, np.abs(W).max() ** 2)
+        # same parameters as the oracle's restatement of _kernels.py:61-81
+        code, cs, sn, ph, t, eta, hyp = O.rotation_params(a, arr, ass, jr == js, 0.0)
+        assert code == 1 and abs(rot.t - t) <= 8 * EPS * max(1.0, abs(t)) and abs(rot.cs - cs) <= 8 * EPS * cs
+
+
+def _correlated_pair(rng, m, b, cplx):
+    """A block pair whose first block is NOT internally orthogonal (columns
+    0 and 1 nearly parallel) and whose second block has a column close to
+    their sum: S = L_j - R_ij^H R_ij of the structured Cholesky
+    (blocking.py:131-134, D = column norms) is indefinite although the pair
+    Gram is positive definite -> the dense fallback (parallel.py:196-198)."""
+    X = rng.standard_normal((m, 2 * b)) + (1j * rng.standard_normal((m, 2 * b)) if cplx else 0)
+    X[:, 1] = X[:, 0] + 1e-3 * X[:, 1]
+    X[:, b] = X[:, 0] + X[:, 1] + 1e-2 * X[:, b]
+    return np.asfortranarray(X)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("b", [16, 64])
+def test_structured_cholesky_fallback_gpu(pkg, torch, cplx, b):
+    rng = np.random.default_rng(21 + b)
+    m = 3 * b
+    G = _correlated_pair(rng, m, b, cplx)
+    J = np.array([1] * (b + 3) + [-1] * (b - 3), np.int8)
+    Gi, Gj = G[:, :b], G[:, b:]
+    with pytest.raises(O.CholeskyFailure):  # the structured path fails on these inputs
+        O.structured_cholesky(O.column_norms2(Gi), O.gram(Gi, Gj), O.column_norms2(Gj))
+    W, R, st, _ = _pivot(pkg, torch, cplx, G, J, items_array([[0, b, b, b]]), b)
+    assert st[0, 4] == 0 and st[0, 7] == 1, st[0]  # status ok, fallback taken
+    # the oracle's pair step takes the same fallback
+    *_, (nrot, nbig, mt, upd, fb) = O.pair_transform(Gi, Gj, O.column_norms2(Gi), O.column_norms2(Gj),
+                                                     J[:b], J[b:], inner_order=_order(pkg, cplx, b))
+    assert fb == 1 and nrot > 0
+    N = 2 * b
+    R0 = O.chol_upper(O.gram(G))
+    Rref = R0.copy(order="F")
+    Wref, *_ = O.diagonalize(Rref, J, order=_order(pkg, cplx, b))
+    lam_g = np.sort(J * O.column_norms2(R[0, :N, :N]))
+    lam_o = np.sort(J * O.column_norms2(Rref))
+    assert np.max(np.abs(lam_g - lam_o) / np.abs(lam_o)) <= 1e-9
+    Wg = W[0, :N, :N]
+    Jf = np.diag(J.astype(float))
+    assert np.abs(Wg.conj().T @ Jf @ Wg - Jf).max() <= 64 * N * EPS * np.linalg.norm(Wg, 2) ** 2
+
+
+def test_rank_deficient_factor_raises_structural(pkg, rng):
+    """Duplicate columns make a pivot singular: the GPU path raises a
+    StructuralError (PivotDefinitenessError(r, s) or DefinitenessError --
+    which one depends on rounding, as in the reference, whose own re-raise
+    fails here: tests/golden/errors.json)."""
+    G = random_full_rank(rng, 16, 16, False)
+    G[:, 9] = G[:, 2]
+    with pytest.raises(pkg.StructuralError) as ei:
+        pkg.parallel_jacobi(G, np.ones(16, np.int8), pkg.SolverConfig(variant="2F", p=2))
+    if isinstance(ei.value, pkg.PivotDefinitenessError):
+        assert 0 <= ei.value.r < ei.value.s
+
+
+@pytest.mark.parametrize("strategy,split", [("round_robin", 3), ("modulus", 4)])
+def test_resume_at_sweep_boundary_is_bitwise(pkg, rng, strategy, split):
+    """Checkpoint/resume (the state at a sweep boundary is G plus
+    the sweep index): sweeps 1..k, then a new call from sweep k+1, gives the
+    uninterrupted solve bit for bit, for odd and even k."""
+    G = random_full_rank(rng, 96, 96, True)
+    J = np.array([1] * 50 + [-1] * 46, np.int8)
+    base = dict(variant="2F", strategy=strategy, p=3, tol=pkg.Tolerances(orth_tol=96 * EPS))
+    full, info = pkg.parallel_jacobi(G, J, pkg.SolverConfig(**base))
+    part, i1 = pkg.parallel_jacobi(G, J, pkg.SolverConfig(**base, sweep_count=split))
+    assert i1.sweeps == split and not i1.converged
+    rest, i2 = pkg.parallel_jacobi(part, J, pkg.SolverConfig(**base, first_sweep=split + 1))
+    assert i2.converged and i2.sweeps == info.sweeps
+    assert np.array_equal(rest, full)
+    assert i1.rotations + i2.rotations == info.rotations

@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
     for name in syms:
         assert hasattr(L, name), name
         assert name in _lib.SIGNATURES, name
-    assert L.hjb_version() == 1
+    assert L.hjb_version() == 2
 
 
 def test_library_is_sm100a():
