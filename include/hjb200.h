@@ -88,6 +88,7 @@ typedef struct {
   int32_t gram_splits;      /* split-K factor of the Gram kernel */
   int64_t inner_sweeps;     /* sum of inner (pivot-level) sweeps over all pivots */
   int64_t inner_pair_visits;/* inner 2x2 pivots examined (sweeps * N(N-1)/2 per pivot) */
+  int64_t kernel_launches;  /* kernels this library launched for the solve (this GPU) */
 } hjb_result;
 
 /* Library / ABI version (HJB_ABI_VERSION). */
@@ -192,6 +193,13 @@ int hjb_tune(int32_t pivot_threads, int32_t pivot_cluster);
  * reference (its inner order is sequential, _kernels.py:41-52); test hook. */
 int hjb_pivot_order(int32_t dtype, int32_t bmax, int32_t count, int32_t cluster, int32_t *nmax,
                     int32_t *warps);
+/* Inner pair order of hjb_pivot / hjb_solve for (dtype, bmax, count,
+ * cluster; 0 = auto): desc int32[5] = (1, NMAX, WARPS, 0, 0) for the round-1
+ * pivot kernel's warp-block order (oracle "wblock:NMAX:WARPS"), or (2, NMAX,
+ * C, W, SPW) for the ring-of-rings Jacobi kernel (oracle
+ * "ror:NMAX:C:W:SPW": the reference's round-robin stepper, strategies.py:
+ * 95-136, over 2CW sub-blocks of SPW columns).  Test hook. */
+int hjb_inner_order(int32_t dtype, int32_t bmax, int32_t count, int32_t cluster, int32_t *desc);
 /* Max co-resident clusters of the pivot kernel instance for (dtype, bmax,
  * cluster, threads) on the current device (negative: cudaError). */
 int hjb_pivot_occupancy(int32_t dtype, int32_t bmax, int32_t cluster, int32_t threads);

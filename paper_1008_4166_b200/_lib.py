@@ -52,6 +52,7 @@ class Result(C.Structure):
         ("exchange_bytes", C.c_int64),
         ("cluster_size", C.c_int32), ("gram_splits", C.c_int32),
         ("inner_sweeps", C.c_int64), ("inner_pair_visits", C.c_int64),
+        ("kernel_launches", C.c_int64),
     ]
 
 
@@ -78,6 +79,7 @@ SIGNATURES = {
     "hjb_pivot_set_profile": (C.c_int, [C.c_void_p]),
     "hjb_tune": (C.c_int, [C.c_int32, C.c_int32]),
     "hjb_pivot_occupancy": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "hjb_inner_order": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "hjb_pivot_order": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                                  C.POINTER(C.c_int32)]),
     "hjb_update": (C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,

@@ -122,5 +122,9 @@ struct Item {
 // per-item pivot statistics, int64 slots (include/hjb200.h hjb_pivot)
 enum { ST_NROT = 0, ST_NBIG, ST_MAXT, ST_SWEEPS, ST_STATUS, ST_FR, ST_FS, ST_FALLBACK, ST_N };
 enum { PV_OK = 0, PV_INDEFINITE = 1, PV_CHOL = 2 };
+// pivot kernel modes: the whole inner level in one kernel (round-1 path), or
+// its prologue (structured Cholesky -> R0) and epilogue (W = R0^-1 R_final)
+// around the Jacobi kernel
+enum { PV_FULL = 0, PV_PROLOGUE = 1, PV_EPILOGUE = 2 };
 
 }  // namespace hjb

@@ -1,0 +1,610 @@
+// Jacobi kernel: the inner level of the 2F step (rotations.py:203-223) as a
+// ring of rings.
+//
+// The pivot factor R (N x N, from the structured Cholesky of the pivot
+// kernel's prologue) is diagonalised by one-sided J-Jacobi sweeps until a
+// sweep applies no rotation.  One thread-block cluster of C CTAs per pivot;
+// every warp of the cluster is a RING WORKER of the reference's own parallel
+// ordering (strategies.py:58-136, round-robin) applied to 2*Q column
+// SUB-BLOCKS of SPW columns (Q = C * W workers):
+//
+//   * a warp holds two sub-blocks (its i and j sub-block, 2*SPW columns) in
+//     registers; lane l holds rows l, l+32, ... of all of them, so a pair's
+//     dot product is a butterfly reduction over the warp and NO column data
+//     moves inside a step;
+//   * step 0 of an inner sweep pairs every two of the warp's own columns
+//     (2*SPW - 1 rounds of SPW disjoint pairs, circle method); every later
+//     step pairs the i sub-block with the j sub-block (SPW rounds);
+//   * after every step the worker's stepper (round_robin_step,
+//     strategies.py:95-136) sends one sub-block to ring neighbour q-1 (odd
+//     inner sweeps) or q+1 (even, strategies.py:69-72) and receives one:
+//     st.async into the neighbour's inbox (shared memory of its CTA, DSMEM
+//     across CTAs) completing on the neighbour's mbarrier; a second mbarrier
+//     per link returns the empty slot.  Warps are coupled only to their ring
+//     neighbours -- there is no CTA or cluster barrier inside a sweep;
+//   * the D cache (rotations.py:217, _kernels.py:80-81) travels with its
+//     column; one cluster reduction of the rotation count per inner sweep is
+//     the convergence test (rotations.py:220-222).
+//
+// Per sweep: (2Q - 1) steps, N - 1 rounds -- every pair of columns meets once
+// (the order is replayed exactly by the oracle, RingOfRings).  Input R0 and
+// output R_final live in global memory ([count][ld*ld], column-major); the
+// pivot kernel forms R0 before and W = R0^-1 R_final after.
+#include <cooperative_groups.h>
+
+#include <cfloat>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+#include <utility>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "rotation.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace hjb {
+
+namespace {
+
+constexpr double kEpsJ = 2.220446049250313e-16;
+
+template <int N, typename F, int... I>
+__device__ __forceinline__ void sfor_impl(F &&f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+// static for: f(integral_constant<0>) ... f(integral_constant<N-1>)
+template <int N, typename F>
+__device__ __forceinline__ void sfor(F &&f) {
+  sfor_impl<N>(static_cast<F &&>(f), std::make_integer_sequence<int, N>{});
+}
+
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
+// Phase-A pairing of the warp's 2*SPW local slots (circle method): round r,
+// pair k -> (slot a, slot b), a < b.
+template <int SPW>
+struct PhaseA {
+  static constexpr int M = 2 * SPW;
+  __host__ __device__ static constexpr int x(int r, int k) { return k == 0 ? M - 1 : (r + k) % (M - 1); }
+  __host__ __device__ static constexpr int y(int r, int k) { return k == 0 ? r : (r - k + (M - 1)) % (M - 1); }
+  __host__ __device__ static constexpr int a(int r, int k) { return x(r, k) < y(r, k) ? x(r, k) : y(r, k); }
+  __host__ __device__ static constexpr int b(int r, int k) { return x(r, k) < y(r, k) ? y(r, k) : x(r, k); }
+};
+
+// mbarrier / DSMEM helpers
+__device__ __forceinline__ void jb_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void jb_arrive_expect(uint64_t *bar, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
+               : "memory");
+}
+// wait for completion of the phase with the given parity (acquire at cluster
+// scope: the data or the empty slot was produced by another CTA)
+__device__ __forceinline__ void jb_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "JB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra JB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t jb_mapa(uint32_t addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void jb_arrive_remote(uint32_t rbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(rbar) : "memory");
+}
+__device__ __forceinline__ void jb_st_async(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void jb_st_async(uint32_t raddr, cplx v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "l"(__double_as_longlong(v.x)), "l"(__double_as_longlong(v.y)), "r"(rbar)
+               : "memory");
+}
+template <int C>
+__device__ __forceinline__ void jb_cluster_sync() {
+  if constexpr (C > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+// round_robin_step of strategies.py:95-136 on one worker's state
+struct Stepper {
+  int ip, jp, ib, jb;  // 1-based, as the reference
+  __device__ __forceinline__ void init(int q, int nbl) {
+    ip = q + 1;
+    jp = nbl - q;
+    ib = ip;
+    jb = jp;
+  }
+  // returns the sent block; ib/jb become the new layout
+  __device__ __forceinline__ int step(int nbl) {
+    int snd;
+    if (ip + jp > nbl) {
+      if (jp < nbl) {
+        snd = ib;
+        ip += 1;
+        if (ip < jp) {
+          ib = ip;
+        } else {
+          ip = jp;
+          ib = jb;
+          jp = nbl;
+          jb = nbl;
+        }
+      } else if (ip > nbl / 2) {
+        snd = ib;
+        ip = ip - nbl / 2 + 1;
+        ib = ip;
+      } else {
+        snd = jb;
+        jp = ip + 1;
+        jb = jp;
+      }
+    } else {
+      snd = jb;
+      jp += 1;
+      jb = jp;
+    }
+    return snd;
+  }
+};
+
+}  // namespace
+
+template <typename T, int N, int C, int W, int SPW>
+struct JacCfg {
+  static constexpr int NT = 32 * W;
+  static constexpr int CPW = 2 * SPW;           // columns per warp
+  static constexpr int RPL = N / 32;             // rows per lane
+  static constexpr int Q = C * W;                // ring workers
+  static constexpr int NBL = 2 * Q;              // sub-blocks
+  static constexpr int LS = ilog2(SPW);
+  static constexpr int GS = 32 >> LS;             // lanes per pair group after the reduce-scatter
+  static constexpr int MSG = SPW * N + SPW;      // inbox message: SPW columns + their D values (elements)
+  static constexpr unsigned MSG_BYTES = MSG * sizeof(T);
+  static_assert(N == 2 * C * W * SPW, "N = 2 C W SPW");
+  static_assert(N % 32 == 0 && (SPW & (SPW - 1)) == 0 && SPW <= 8, "shape");
+  // shared memory: inbox [W][2][MSG] T, full/empty barriers [W][2], J [N]
+  static constexpr size_t OFF_IN = 0;
+  static constexpr size_t OFF_BAR = OFF_IN + size_t(W) * 2 * MSG * sizeof(T);
+  static constexpr size_t OFF_J = OFF_BAR + size_t(W) * 4 * sizeof(uint64_t);
+  static constexpr size_t SMEM = OFF_J + N * sizeof(int);
+};
+
+template <typename T, int N, int C, int W, int SPW, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
+  using Cfg = JacCfg<T, N, C, W, SPW>;
+  constexpr int RPL = Cfg::RPL, CPW = Cfg::CPW, Q = Cfg::Q, NBL = Cfg::NBL, LS = Cfg::LS, GS = Cfg::GS;
+  constexpr int MSG = Cfg::MSG;
+  extern __shared__ __align__(16) unsigned char smem[];
+  T *inbox = reinterpret_cast<T *>(smem + Cfg::OFF_IN);         // [W][2][MSG]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Cfg::OFF_BAR);  // [W][full 2, empty 2]
+  int *Jv = reinterpret_cast<int *>(smem + Cfg::OFF_J);
+  __shared__ int s_cnt[2], s_big[2], s_fail[2];
+  __shared__ unsigned long long s_maxt;
+
+  int crank = 0;
+  if constexpr (C > 1) crank = int(cg::this_cluster().block_rank());
+  const int item_id = blockIdx.x / C;
+  const Item it = a.items[item_id];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = crank * W + warp;  // ring worker
+  const int ni = it.ni, nj = it.nj, Nq = ni + nj;
+  int64_t *st = a.stats + int64_t(item_id) * ST_N;
+  // the prologue failed (DefinitenessError): nothing to diagonalise
+  if (__ldcg(st + ST_STATUS) != PV_OK) return;  // uniform over the cluster
+  const int ld = a.ld;
+  const T *R0 = reinterpret_cast<const T *>(a.R0) + int64_t(item_id) * ld * ld;
+  T *Rf = reinterpret_cast<T *>(a.Rout) + int64_t(item_id) * ld * ld;
+
+  for (int c = tid; c < N; c += Cfg::NT)
+    Jv[c] = c < ni ? a.signs[it.oi + c] : (c < Nq ? a.signs[it.oj + (c - ni)] : 1);
+  if (tid < 2 * W) {
+    jb_init(&bars[(tid >> 1) * 4 + (tid & 1)], 1);      // full[dir]: the receiver's expect_tx arrival
+    jb_init(&bars[(tid >> 1) * 4 + 2 + (tid & 1)], 1);  // empty[dir]: the receiver's remote arrival
+  }
+  if (tid == 0) {
+    s_cnt[0] = s_cnt[1] = 0;
+    s_big[0] = s_big[1] = 0;
+    s_fail[0] = s_fail[1] = INT_MAX;
+    s_maxt = 0ull;
+  }
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+
+  // ---- this worker's two sub-blocks, rows lane + 32u ----
+  Stepper sp;
+  sp.init(q, NBL);
+  T V[RPL][CPW];
+  double D[CPW] = {};
+  auto col_of = [&](int slot) { return (slot < SPW ? (sp.ib - 1) * SPW + slot : (sp.jb - 1) * SPW + slot - SPW); };
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const int col = col_of(c);
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) V[u][c] = __ldcg(R0 + (lane + 32 * u) + int64_t(col) * ld);
+  }
+  jb_cluster_sync<C>();  // Jv, barriers initialised in every CTA
+
+  const double otol = a.orth_tol > 0.0 ? a.orth_tol : sqrt(double(Nq)) * kEpsJ;
+  const double otol2 = otol * otol;
+  const double qtol = a.quad_tol > 0.0 ? a.quad_tol : double(Nq) * kEpsJ;
+  int my_cnt = 0, my_big = 0, my_fail = INT_MAX;
+  double my_maxt = 0.0;
+  long long nrot_total = 0, big_total = 0;
+  int sweeps = 0, status = PV_OK;
+  int gdir[2] = {0, 0};  // messages sent/received per direction (equal in every worker)
+
+  // -------------------------------------------------------------- one round
+  // pairs (slot A(k), slot B(k)), k < SPW, of this warp; A plays r, B plays s
+  auto round = [&](auto pa, auto pb) {
+    T dp[SPW];
+    sfor<SPW>([&](auto k) {
+      constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
+      T d0 = S<T>::zero(), d1 = S<T>::zero();
+#pragma unroll
+      for (int u = 0; u < RPL; u += 2) {
+        d0 = cfma(V[u][A], V[u][B], d0);
+        if (u + 1 < RPL) d1 = cfma(V[u + 1][A], V[u + 1][B], d1);
+      }
+      dp[k] = add(d0, d1);
+    });
+    // butterfly reduce-scatter: lane keeps pair kk = lane >> (5 - S)
+#pragma unroll
+    for (int j = 0; j < LS; ++j) {
+      const int dist = 16 >> j;
+      const bool hi = lane & dist;
+      const int half = SPW >> (j + 1);
+#pragma unroll
+      for (int x = 0; x < half; ++x) {
+        const T snd = hi ? dp[x] : dp[x + half];
+        const T keep = hi ? dp[x + half] : dp[x];
+        dp[x] = add(keep, shfl_xor(snd, dist));
+      }
+    }
+    T acc = dp[0];
+#pragma unroll
+    for (int dist = 16 >> LS; dist >= 1; dist >>= 1) acc = add(acc, shfl_xor(acc, dist));
+    const int kk = lane >> (5 - LS);
+    // this lane's pair: D values, signs, column ids
+    double dr = 0.0, ds = 0.0;
+    int sr = 1, ss = 1, cr = 0, cs = 0;
+    sfor<SPW>([&](auto k) {
+      constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
+      if (kk == k) {
+        dr = D[A];
+        ds = D[B];
+        cr = col_of(A);
+        cs = col_of(B);
+      }
+    });
+    sr = Jv[cr];
+    ss = Jv[cs];
+    bool rot = cr < Nq && cs < Nq && !(abs2(acc) <= otol2 * (dr * ds));  // _kernels.py:57
+    RotCoef<T> p;
+    p.cp = S<T>::one();
+    p.sp = S<T>::zero();
+    p.hs = 0.0;
+    p.cs = 1.0;
+    double te_n = 0.0, te_d = 1.0, te_h = 0.0;
+    if (__any_sync(0xffffffffu, rot)) {
+      if (rot) {
+        const RotCoef<T> r = rot_coef<T>(acc, dr, ds, sr == ss, otol2);
+        if (r.code == 1) {
+          p = r;
+          te_n = r.num * r.eta;
+          te_d = r.den;
+          te_h = r.hyp;
+          if ((lane & (GS - 1)) == 0) {
+            ++my_cnt;
+            const double t = fabs(r.num) / r.den;
+            my_big += fabs(r.num) > qtol * r.den;  // |t| > quad_tol
+            my_maxt = fmax(my_maxt, t);
+          }
+        } else {
+          rot = false;
+          if (r.code < 0 && (lane & (GS - 1)) == 0) my_fail = min(my_fail, min(cr, cs) * 4096 + max(cr, cs));
+        }
+      }
+      // every lane applies every pair of the warp: parameters of pair k from
+      // the first lane of its group
+      sfor<SPW>([&](auto k) {
+        constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
+        const int src = k * GS;
+        const bool rk = __shfl_sync(0xffffffffu, rot, src);
+        if (rk) {
+          RotCoef<T> pk;
+          pk.cp = shfl_idx(p.cp, src);
+          pk.sp = shfl_idx(p.sp, src);
+          pk.hs = __shfl_sync(0xffffffffu, p.hs, src);
+          pk.cs = __shfl_sync(0xffffffffu, p.cs, src);
+          const double tn = __shfl_sync(0xffffffffu, te_n, src);
+          const double td = __shfl_sync(0xffffffffu, te_d, src);
+          const double th = __shfl_sync(0xffffffffu, te_h, src);
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) rot_fold<T>(V[u][A], V[u][B], pk);
+          const double te = tn / td;  // t * eta (_kernels.py:80-81)
+          D[A] = fma(th, te, D[A]);
+          D[B] = D[B] + te;
+        }
+      });
+    }
+  };
+
+  // phase A: all pairs of the warp's 2 SPW columns; phase B: i x j
+  auto phase_a = [&]() {
+    sfor<CPW - 1>([&](auto r) {
+      constexpr int R = decltype(r)::value;
+      round([](auto k) { return std::integral_constant<int, PhaseA<SPW>::a(R, decltype(k)::value)>{}; },
+            [](auto k) { return std::integral_constant<int, PhaseA<SPW>::b(R, decltype(k)::value)>{}; });
+    });
+  };
+  auto phase_b = [&]() {
+    sfor<SPW>([&](auto r) {
+      constexpr int R = decltype(r)::value;
+      round([](auto k) { return std::integral_constant<int, decltype(k)::value>{}; },
+            [](auto k) { return std::integral_constant<int, SPW + (decltype(k)::value + R) % SPW>{}; });
+    });
+  };
+
+  // ---------------------------------------------------------- the exchange
+  // strategies.py:69-72: odd sweeps send to q-1 and receive from q+1
+  auto exchange = [&](int nsweep) {
+    const int old_i = sp.ib, old_j = sp.jb;
+    const int snd = sp.step(NBL);
+    const bool send_i = snd == old_i;
+    const bool swap = send_i && sp.ib == old_j;  // j moved into the i slots, receive into j
+    const int d = (nsweep & 1) ? 0 : 1;
+    const int dst = (nsweep & 1) ? (q + Q - 1) % Q : (q + 1) % Q;
+    const int srcw = (nsweep & 1) ? (q + 1) % Q : (q + Q - 1) % Q;
+    const int g = gdir[d]++;
+    uint64_t *full = &bars[warp * 4 + d];
+    uint64_t *empty = &bars[warp * 4 + 2 + d];
+    // send: wait until the receiver has consumed this link's previous message
+    if (g > 0) jb_wait(empty, (g - 1) & 1);
+    {
+      const int dc = dst / W, dw = dst % W;
+      T *box = inbox + (size_t(dw) * 2 + d) * MSG;
+      const uint32_t rbox = jb_mapa(smem_u32(box), dc);
+      const uint32_t rbar = jb_mapa(smem_u32(&bars[dw * 4 + d]), dc);
+      sfor<SPW>([&](auto k) {
+        constexpr int K = decltype(k)::value;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const T v = send_i ? V[u][K] : V[u][SPW + K];
+          jb_st_async(rbox + uint32_t((K * N + lane + 32 * u) * sizeof(T)), v, rbar);
+        }
+      });
+      if (lane < SPW) {
+        double dv = 0.0;
+        sfor<SPW>([&](auto k) {
+          if (lane == decltype(k)::value) dv = send_i ? D[decltype(k)::value] : D[SPW + decltype(k)::value];
+        });
+        jb_st_async(rbox + uint32_t((SPW * N + lane) * sizeof(T)), scale(S<T>::one(), dv), rbar);
+      }
+    }
+    // receive into the vacated slots
+    if (swap) {
+      sfor<SPW>([&](auto k) {
+        constexpr int K = decltype(k)::value;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) V[u][K] = V[u][SPW + K];
+        D[K] = D[SPW + K];
+      });
+    }
+    if (lane == 0) jb_arrive_expect(full, Cfg::MSG_BYTES);
+    jb_wait(full, g & 1);
+    const T *box = inbox + (size_t(warp) * 2 + d) * MSG;
+    const bool into_i = send_i && !swap;
+    sfor<SPW>([&](auto k) {
+      constexpr int K = decltype(k)::value;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const T v = box[K * N + lane + 32 * u];
+        if (into_i) V[u][K] = v; else V[u][SPW + K] = v;
+      }
+      const double dv = re(box[SPW * N + K]);
+      if (into_i) D[K] = dv; else D[SPW + K] = dv;
+    });
+    __syncwarp();
+    if (lane == 0) {
+      const int sc = srcw / W, sw = srcw % W;
+      jb_arrive_remote(jb_mapa(smem_u32(&bars[sw * 4 + 2 + d]), sc));
+    }
+  };
+
+  // ---------------------------------------------------------- inner sweeps
+  for (int sw = 0; sw < a.max_sweeps; ++sw) {
+    const int nsweep = sw + 1;  // the reference counts sweeps from 1
+    ++sweeps;
+    // D = colnorms^2(R) (rotations.py:217): butterfly all-reduce per column
+    {
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; u += 2) {
+          s0 += abs2(V[u][c]);
+          if (u + 1 < RPL) s1 += abs2(V[u + 1][c]);
+        }
+        D[c] = s0 + s1;
+      }
+#pragma unroll
+      for (int dist = 16; dist >= 1; dist >>= 1)
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) D[c] += __shfl_xor_sync(0xffffffffu, D[c], dist);
+    }
+    phase_a();
+    for (int s = 1; s < NBL - 1; ++s) {
+      exchange(nsweep);
+      phase_b();
+    }
+    // ---- sweep end: cluster-wide rotation count (parallel.py:239-244 at the
+    // inner level, rotations.py:220-222) ----
+    const int par = sw & 1;
+    {
+      const int wc = __reduce_add_sync(0xffffffffu, my_cnt);
+      const int wb = __reduce_add_sync(0xffffffffu, my_big);
+      const int wf = __reduce_min_sync(0xffffffffu, my_fail);
+      if (lane == 0) {
+        if (wc) atomicAdd(&s_cnt[par], wc);
+        if (wb) atomicAdd(&s_big[par], wb);
+        if (wf != INT_MAX) atomicMin(&s_fail[par], wf);
+      }
+      my_cnt = my_big = 0;
+    }
+    jb_cluster_sync<C>();
+    long long tot = 0;
+    int big = 0, fl = INT_MAX;
+#pragma unroll
+    for (int r = 0; r < C; ++r) {
+      const int *pc = C > 1 ? cg::this_cluster().map_shared_rank(&s_cnt[par], r) : &s_cnt[par];
+      const int *pb = C > 1 ? cg::this_cluster().map_shared_rank(&s_big[par], r) : &s_big[par];
+      const int *pf = C > 1 ? cg::this_cluster().map_shared_rank(&s_fail[par], r) : &s_fail[par];
+      tot += *pc;
+      big += *pb;
+      fl = min(fl, *pf);
+    }
+    if (tid == 0) {  // reset the other parity for the next sweep (read only after the next cluster sync)
+      s_cnt[par ^ 1] = 0;
+      s_big[par ^ 1] = 0;
+      s_fail[par ^ 1] = INT_MAX;
+    }
+    big_total += big;
+    nrot_total += tot;
+    if (fl != INT_MAX) {
+      status = PV_INDEFINITE;
+      my_fail = fl;
+      break;
+    }
+    if (tot == 0 || sw + 1 == a.max_sweeps) break;
+    exchange(nsweep);  // the sweep's last exchange (parallel.py:234-237)
+  }
+  // max |t| over the cluster
+  if (my_maxt > 0.0) atomicMax(&s_maxt, static_cast<unsigned long long>(__double_as_longlong(my_maxt)));
+  // ---- R_final -> global (column ids travel with the sub-blocks) ----
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const int col = col_of(c);
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) Rf[(lane + 32 * u) + int64_t(col) * ld] = V[u][c];
+  }
+  jb_cluster_sync<C>();
+  if (tid == 0) {
+    unsigned long long mt = s_maxt;
+#pragma unroll
+    for (int r = 0; r < C; ++r) {
+      const unsigned long long *pm = C > 1 ? cg::this_cluster().map_shared_rank(&s_maxt, r) : &s_maxt;
+      mt = max(mt, *pm);
+    }
+    if (crank == 0) {
+      st[ST_NROT] = nrot_total;
+      st[ST_NBIG] = big_total;
+      st[ST_MAXT] = static_cast<int64_t>(mt);
+      st[ST_SWEEPS] = sweeps;
+      st[ST_STATUS] = status;
+      st[ST_FR] = status == PV_INDEFINITE ? my_fail / 4096 : -1;
+      st[ST_FS] = status == PV_INDEFINITE ? my_fail % 4096 : -1;
+    }
+  }
+  jb_cluster_sync<C>();  // peers' shared memory stays alive until read
+}
+
+// ------------------------------------------------------------------ launch
+
+template <typename T, int N, int C, int W, int SPW>
+static cudaError_t launch_jacobi_t(const JacobiArgs &a, cudaStream_t st) {
+  using Cfg = JacCfg<T, N, C, W, SPW>;
+  // two CTAs per SM when the register-resident columns allow it
+  constexpr int REGS = 2 * Cfg::RPL * Cfg::CPW * int(sizeof(T) / 8);
+  constexpr int MINB = REGS <= 64 ? 2 : 1;
+  auto k = jacobi_kernel<T, N, C, W, SPW, MINB>;
+  static DeviceFlags attr_flags;
+  bool *attr = attr_flags.here();
+  if (!attr) return cudaErrorInvalidDevice;
+  if (!*attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));
+    if (e != cudaSuccess) return e;
+    if (C > 8) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    *attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.count * C);
+  cfg.blockDim = dim3(Cfg::NT);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = C;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+// instantiated shapes: (N, C, W, SPW) with N = 2 C W SPW
+#define HJB_JAC_SHAPES(X)                                                                              \
+  X(32, 1, 4, 4) X(32, 2, 4, 2) X(64, 2, 4, 4) X(64, 4, 4, 2) X(128, 4, 8, 2) X(128, 8, 4, 2)         \
+  X(128, 4, 4, 4) X(256, 8, 8, 2) X(256, 4, 8, 4) X(256, 16, 4, 2)
+
+JacShape jacobi_default_shape(bool cx, int nmax, int count) {
+  static int ov_c = -1, ov_w = 0, ov_s = 0;
+  if (ov_c < 0) {  // experiments: HJB_JAC_SHAPE="C,W,SPW"
+    ov_c = 0;
+    if (const char *e = std::getenv("HJB_JAC_SHAPE")) sscanf(e, "%d,%d,%d", &ov_c, &ov_w, &ov_s);
+  }
+  if (ov_c > 0 && 2 * ov_c * ov_w * ov_s == nmax) return JacShape{ov_c, ov_w, ov_s};
+  (void)cx;
+  (void)count;
+  switch (nmax) {
+    case 32: return JacShape{1, 4, 4};
+    case 64: return JacShape{2, 4, 4};
+    case 128: return JacShape{8, 4, 2};
+    case 256: return JacShape{8, 8, 2};
+  }
+  return JacShape{0, 0, 0};
+}
+
+bool jacobi_shape_for(int nmax, int c, JacShape *out) {
+#define HJB_JAC_FIND(N_, C_, W_, S_)          \
+  if (nmax == N_ && c == C_) {                \
+    *out = JacShape{C_, W_, S_};              \
+    return true;                              \
+  }
+  HJB_JAC_SHAPES(HJB_JAC_FIND)
+#undef HJB_JAC_FIND
+  return false;
+}
+
+template <typename T>
+static cudaError_t dispatch_jacobi(const JacobiArgs &a, JacShape s, cudaStream_t st) {
+#define HJB_JAC_CASE(N_, C_, W_, S_)                                              \
+  if (a.nmax == N_ && s.c == C_ && s.w == W_ && s.spw == S_) return launch_jacobi_t<T, N_, C_, W_, S_>(a, st);
+  HJB_JAC_SHAPES(HJB_JAC_CASE)
+#undef HJB_JAC_CASE
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_jacobi(bool cx, const JacobiArgs &a, JacShape s, cudaStream_t st) {
+  if (a.count == 0) return cudaSuccess;
+  return cx ? dispatch_jacobi<cplx>(a, s, st) : dispatch_jacobi<double>(a, s, st);
+}
+
+}  // namespace hjb

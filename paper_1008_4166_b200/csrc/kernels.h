@@ -41,6 +41,8 @@ struct PivotArgs {
   long long *prof;    // optional per-CTA phase clocks [count*C][8] (debug)
   void *uscr;         // [count][nmax/2][nmax/2+1] factor U of the fast path (L2 scratch)
   void *gchk;         // [count][16][blocks][16] Gram-check partials (L2 scratch), may be null
+  int mode;           // PV_FULL: whole pivot; PV_PROLOGUE: R0 -> R0g only; PV_EPILOGUE: W = R0^-1 R_final
+  void *R0g;          // [count][nmax*nmax] R0 (prologue output / epilogue input)
 };
 // cluster: 0 = automatic choice
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used);
@@ -56,6 +58,25 @@ int pivot_choose_threads(bool cx, int nmax, int c);  // Gram-check scratch eleme
 
 cudaError_t launch_plane_rotations(bool cx, int count, const double *arr, const double *ass, const void *ars,
                                    const int8_t *same, double *out, cudaStream_t st);
+
+// Jacobi kernel (jacobi.cu): R0 -> R_final for a batch of pivots.
+struct JacobiArgs {
+  const Item *items;
+  int count;
+  int nmax, ld;          // pivot order instance and leading dimension of R0 / Rout
+  const void *R0;        // [count][ld*ld] initial factor (pivot kernel prologue)
+  void *Rout;            // [count][ld*ld] final factor
+  const int8_t *signs;
+  double orth_tol, quad_tol;
+  int max_sweeps;
+  int64_t *stats;        // [count][ST_N]: status/fallback in, counters out
+};
+struct JacShape {
+  int c, w, spw;  // cluster size, warps per CTA, pairs per warp (nmax = 2 c w spw)
+};
+JacShape jacobi_default_shape(bool cx, int nmax, int count);
+bool jacobi_shape_for(int nmax, int c, JacShape *out);  // an instantiated shape with cluster size c
+cudaError_t launch_jacobi(bool cx, const JacobiArgs &a, JacShape s, cudaStream_t st);
 
 struct UpdateArgs {
   void *G;

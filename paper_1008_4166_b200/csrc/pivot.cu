@@ -34,6 +34,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "rotation.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -186,80 +187,6 @@ __device__ __forceinline__ void st_shared_if(bool p, cplx *dst, cplx v) {
                : "memory");
 }
 
-// Rotation coefficients with the phase folded in: [x_r, x_s] <-
-// [cp x_r + hs x_s, sp x_r + cs x_s], cp = cs*phase, sp = sn*phase,
-// hs = hyp*sn -- algebraically _kernels.py:82-92.
-template <typename T>
-struct RotCoef {
-  int code;  // 0 skip, 1 rotate, -1 indefinite pivot
-  double cs, hs, num, den, eta, hyp;  // t = num / den (kept off the dependency chain)
-  T cp, sp;
-};
-
-__device__ __forceinline__ double phase_mul(double a, double s) { return a * s; }
-__device__ __forceinline__ cplx phase_mul(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
-
-// _kernels.py:53-81 restated for a short dependency chain.  With q = |a|^2,
-// e = 2*eta (e^2 = 4q) and delta = d_s - d_r:
-//   trig:       t = sgn(theta)|e| / (|delta| + sqrt(delta^2 + 4q))
-//   hyperbolic: t = -e / (s + sqrt(s^2 - 4q)),  s = d_r + d_s
-// and cs = den / sqrt(den^2 +- 4q), sn = num / sqrt(den^2 +- 4q).  The chain
-// is q -> sqrt -> rsqrt (|a| and the phase come from an independent rsqrt);
-// s^2 - 4q and den^2 - 4q are single-rounding FMAs.
-template <typename T>
-__device__ __forceinline__ RotCoef<T> rot_coef(T a, double dr, double ds, bool same, double otol2) {
-  // branch-free: both rotation kinds share den = |x| + sqrt(x^2 +- 4q),
-  // r = rsqrt(den^2 +- 4q) with x = d_s - d_r (trig, +) or d_r + d_s (hyp, -)
-  RotCoef<T> p;
-  const double q = abs2(a);
-  const double dd = dr * ds;
-  const double q4 = 4.0 * q;
-  const double ri = rsqrt(q);
-  const double sa = re(a) >= 0.0 ? 1.0 : -1.0;
-  const double aa = q * ri;
-  const double x = same ? ds - dr : dr + ds;
-  const double sq4 = same ? q4 : -q4;
-  const double disc = fma(x, x, sq4);
-  const double den = fabs(x) + sqrt(fmax(disc, 0.0));
-  const double r = rsqrt(fma(den, den, sq4));
-  const bool pos = x == 0.0 || ((x > 0.0) == (sa > 0.0));
-  const double num = same ? (pos ? 2.0 * aa : -2.0 * aa) : -2.0 * sa * aa;
-  const bool skip = q <= otol2 * dd;                     // _kernels.py:57
-  const bool bad = q >= dd || (!same && disc <= 0.0);   // _kernels.py:59-60, 73-74
-  p.code = skip ? 0 : (bad ? -1 : 1);
-  p.hyp = same ? -1.0 : 1.0;
-  const double cs = den * r, sn = num * r;
-  const T ph = phase_mul(a, sa * ri);
-  p.cs = cs;
-  p.hs = p.hyp * sn;
-  p.cp = phase_mul(ph, cs);
-  p.sp = phase_mul(ph, sn);
-  p.num = num;
-  p.den = den;
-  p.eta = sa * aa;
-  return p;
-}
-
-template <typename T>
-__device__ __forceinline__ void rot_fold(T &xr, T &xs, const RotCoef<T> &p);
-template <>
-__device__ __forceinline__ void rot_fold<double>(double &xr, double &xs, const RotCoef<double> &p) {
-  const double nr = fma(p.cp, xr, p.hs * xs);
-  const double ns = fma(p.sp, xr, p.cs * xs);
-  xr = nr;
-  xs = ns;
-}
-template <>
-__device__ __forceinline__ void rot_fold<cplx>(cplx &xr, cplx &xs, const RotCoef<cplx> &p) {
-  cplx nr, ns;
-  nr.x = fma(p.cp.x, xr.x, fma(-p.cp.y, xr.y, p.hs * xs.x));
-  nr.y = fma(p.cp.x, xr.y, fma(p.cp.y, xr.x, p.hs * xs.y));
-  ns.x = fma(p.sp.x, xr.x, fma(-p.sp.y, xr.y, p.cs * xs.x));
-  ns.y = fma(p.sp.x, xr.y, fma(p.sp.y, xr.x, p.cs * xs.y));
-  xr = nr;
-  xs = ns;
-}
-
 // compute_plane_rotation (rotations.py:128-155) for a batch of 2x2 Gram
 // pivots [[a_rr, a_rs], [conj(a_rs), a_ss]] through the pivot kernel's own
 // rot_coef (no skip threshold: only a_rs == 0 is the identity).  out[k] =
@@ -369,6 +296,25 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   bool fast = false;
   const int nt = dense ? 0 : ni;  // rows of R0 with the diagonal sqrt(L_i) block
   const int nu = dense ? N : nj;  // order of U
+  const int mode = a.mode;
+  T *R0g = a.R0g ? reinterpret_cast<T *>(a.R0g) + int64_t(item_id) * a.nmax * a.nmax : nullptr;
+  if (mode == PV_EPILOGUE) {
+    // W = R0^-1 R_final after the Jacobi kernel: R_final is in W, R0 in R0g
+    // (the U factor of the fast path in the L2 scratch); nothing to do for a
+    // failed pivot or one that applied no rotation (the update skips it)
+    const int64_t *sv = a.stats + int64_t(item_id) * ST_N;
+    status = int(__ldcg(sv + ST_STATUS));
+    fallback = int(__ldcg(sv + ST_FALLBACK));
+    if (status != PV_OK || __ldcg(sv + ST_NROT) == 0) return;  // uniform over the cluster
+    fast = Cfg::FAST && !fallback;
+    if (!fast) {
+      for (int e = tid; e < RPC * NMAX; e += NT) {
+        const int gl = e % RPC, c = e / RPC;
+        Rs[gl + c * RS] = __ldcg(R0g + (row0 + gl) + int64_t(c) * a.nmax);
+      }
+      __syncthreads();
+    }
+  } else {
   if constexpr (Cfg::FAST) {
     int ok = 1;
     if (!dense) {
@@ -692,6 +638,31 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     __syncthreads();
     if (!cholesky(0)) status = PV_CHOL;
   }
+  }  // mode != PV_EPILOGUE
+
+  if (mode == PV_PROLOGUE) {
+    // R0 (whole N x N, zero padded) -> global for the Jacobi kernel; status
+    // and fallback for it and the epilogue
+    if (status == PV_OK)
+      for (int e = tid; e < RPC * a.nmax; e += NT) {
+        const int gl = e % RPC, c = e / RPC;
+        const int g = row0 + gl;
+        if (g < a.nmax) R0g[g + int64_t(c) * a.nmax] = c < NMAX ? Rs[gl + c * RS] : S<T>::zero();
+      }
+    if (crank == 0 && tid == 0) {
+      int64_t *st = a.stats + int64_t(item_id) * ST_N;
+      st[ST_NROT] = 0;
+      st[ST_NBIG] = 0;
+      st[ST_MAXT] = 0;
+      st[ST_SWEEPS] = 0;
+      st[ST_STATUS] = status;
+      st[ST_FR] = -1;
+      st[ST_FS] = -1;
+      st[ST_FALLBACK] = fallback;
+    }
+    cluster_sync<C>();  // peers' shared memory stays alive until every remote read is done
+    return;
+  }
 
   t_chol = clock64();
   // ------------------------------------------------------------------ Jacobi
@@ -883,7 +854,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     if (tid == 0) s_flag[1] = 0;
     return ok;
   };
-  if (status == PV_OK) {
+  if (status == PV_OK && mode == PV_FULL) {
     for (int sw = 0; sw < a.max_sweeps; ++sw) {
       ++sweeps;
       // A sweep after one whose rotations were all tiny is almost surely the
@@ -1228,7 +1199,14 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
         for (int e = tid; e < Cfg::UB * UL; e += NT) Rs[e] = __ldcg(Ug + e);
       }
       const T *U = Cfg::U_SMEM ? Rs : Ug;
-      if (in_ring) {
+      if (mode == PV_EPILOGUE && Rout) {  // R_final (from the Jacobi kernel) for the optional output
+        for (int e = tid; e < RPC * N; e += NT) {
+          const int gl = e % RPC, c = e / RPC;
+          const int g = row0 + gl;
+          if (g < N) Rout[g + int64_t(c) * nmax] = __ldcg(Wout + g + int64_t(c) * nmax);
+        }
+      }
+      if (mode == PV_FULL && in_ring) {
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
           const int g = row0 + lane_in + u * TPP;
@@ -1321,9 +1299,16 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
   if (!fast) {
     T *Fs = Ws;  // RPC x NMAX slab (scratch region is large enough)
     __syncthreads();
+    if (mode == PV_EPILOGUE) {  // R_final rows of this CTA from the Jacobi kernel's output
+      for (int e = tid; e < RPC * NMAX; e += NT) {
+        const int gl = e % RPC, c = e / RPC;
+        const int g = row0 + gl;
+        Fs[c * RS + gl] = (g < N && c < N) ? __ldcg(Wout + g + int64_t(c) * nmax) : S<T>::zero();
+      }
+    }
   #pragma unroll
     for (int u = 0; u < RPT; ++u) {
-      if (!in_ring) break;
+      if (!in_ring || mode != PV_FULL) break;
       const int row = lane_in + u * TPP;
       Fs[cX * RS + row] = X[u];
       Fs[cY * RS + row] = Y[u];
@@ -1420,7 +1405,7 @@ __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
     long long *pp = a.prof + int64_t(gridDim.x) * 8 + int64_t(blockIdx.x) * 8;
     for (int i = 0; i < 8; ++i) pp[i] = ph[i];
   }
-  if (crank == 0 && tid == 0) {
+  if (crank == 0 && tid == 0 && mode == PV_FULL) {
     int64_t *st = a.stats + int64_t(item_id) * ST_N;
     st[ST_NROT] = nrot_total;
     st[ST_NBIG] = s_big;

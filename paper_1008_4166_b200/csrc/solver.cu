@@ -82,7 +82,7 @@ struct HBuf {
 };
 
 struct Workspace {
-  DBuf G, items, A, D, W, U, Gc, stats, signs, red, lam, flag;
+  DBuf G, items, A, D, W, U, Gc, R0, stats, signs, red, lam, flag;
   HBuf stats_h, red_h;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> events;
@@ -136,6 +136,50 @@ int gram_splits(int count, int tiles, int64_t m, int kc, int64_t *ksplit) {
   return s;
 }
 
+// Inner level: the ring-of-rings Jacobi kernel between the pivot kernel's
+// prologue and epilogue (default), or the round-1 single pivot kernel
+// (HJB_PIVOT_V1=1, kept for A/B measurements).
+bool inner_v1() {
+  static const bool v1 = [] {
+    const char *e = std::getenv("HJB_PIVOT_V1");
+    return e && std::atoi(e) != 0;
+  }();
+  return v1;
+}
+
+// the three pivot-phase launches of one batch (or the single v1 launch)
+cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st, int *cluster_used, int *launches) {
+  if (inner_v1()) {
+    pa.mode = PV_FULL;
+    ++*launches;
+    return launch_pivot(cx, pa, cluster_req, st, cluster_used);
+  }
+  pa.mode = PV_PROLOGUE;
+  cudaError_t e = launch_pivot(cx, pa, 0, st, nullptr);
+  if (e != cudaSuccess) return e;
+  JacobiArgs j{};
+  j.items = pa.items;
+  j.count = pa.count;
+  j.nmax = pa.nmax;
+  j.ld = pa.nmax;
+  j.R0 = pa.R0g;
+  j.Rout = pa.W;
+  j.signs = pa.signs;
+  j.orth_tol = pa.orth_tol;
+  j.quad_tol = pa.quad_tol;
+  j.max_sweeps = pa.max_sweeps;
+  j.stats = pa.stats;
+  JacShape sh = jacobi_default_shape(cx, pa.nmax, pa.count);
+  if (cluster_req > 0 && cluster_req != sh.c && !jacobi_shape_for(pa.nmax, cluster_req, &sh))
+    return cudaErrorInvalidConfiguration;  // no instantiated shape with that cluster size
+  if (cluster_used) *cluster_used = sh.c;
+  e = launch_jacobi(cx, j, sh, st);
+  if (e != cudaSuccess) return e;
+  pa.mode = PV_EPILOGUE;
+  *launches += 3;
+  return launch_pivot(cx, pa, 0, st, nullptr);
+}
+
 struct PhaseCtx {
   bool cx;
   int64_t m, ld;
@@ -147,6 +191,7 @@ struct PhaseCtx {
   Workspace *ws;
   cudaStream_t st;
   int splits_used = 0;
+  int launches = 0;  // kernels launched by this solve
 };
 
 // Gram -> pivot -> update for one batch of items (device item table).
@@ -171,6 +216,7 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   g.D = static_cast<double *>(c.ws->D.p);
   if (ev) CK(cudaEventRecord(ev[0], c.st));
   CK(launch_gram(c.cx, g, c.st));
+  ++c.launches;
   if (ev) CK(cudaEventRecord(ev[1], c.st));
   PivotArgs pa{};
   pa.G = c.G;
@@ -191,8 +237,9 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   pa.nmax = c.nmax;
   pa.uscr = c.ws->U.p;
   pa.gchk = c.ws->Gc.p;
+  pa.R0g = c.ws->R0.p;
   int used = 0;
-  CK(launch_pivot(c.cx, pa, c.cluster_req, c.st, &used));
+  CK(launch_inner(c.cx, pa, c.cluster_req, c.st, &used, &c.launches));
   c.cluster = used;
   if (ev) CK(cudaEventRecord(ev[2], c.st));
   UpdateArgs u{};
@@ -205,6 +252,7 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   u.W = c.ws->W.p;
   u.stats = stats_d;
   CK(launch_update(c.cx, u, c.st));
+  ++c.launches;
   if (ev) CK(cudaEventRecord(ev[3], c.st));
   return HJB_OK;
 }
@@ -217,6 +265,7 @@ int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_co
   CK(ws.W.reserve(size_t(max_count) * nmax * nmax * w));
   CK(ws.U.reserve(size_t(max_count) * (nmax / 2) * (nmax / 2 + 1) * w));  // pivot factor U (L2 scratch)
   CK(ws.Gc.reserve(size_t(max_count) * pivot_check_elems(nmax) * w));    // final-sweep Gram check
+  CK(ws.R0.reserve(size_t(max_count) * nmax * nmax * w));                 // R0 between prologue and Jacobi
   return HJB_OK;
 }
 
@@ -360,6 +409,29 @@ int hjb_pivot_order(int32_t dtype, int32_t bmax, int32_t count, int32_t cluster,
   const int c = cluster > 0 ? cluster : pivot_choose_cluster(cx, nm, count);
   *nmax = nm;
   *warps = pivot_choose_threads(cx, nm, c) / 32;
+  return HJB_OK;
+}
+
+int hjb_inner_order(int32_t dtype, int32_t bmax, int32_t count, int32_t cluster, int32_t *desc) {
+  const bool cx = dtype == HJB_C128;
+  const int nm = pivot_nmax(bmax);
+  if (nm < 0 || count < 1 || !desc) return fail(HJB_EINVAL, "hjb_inner_order: bad arguments");
+  if (inner_v1()) {
+    const int c = cluster > 0 ? cluster : pivot_choose_cluster(cx, nm, count);
+    desc[0] = 1;
+    desc[1] = nm;
+    desc[2] = pivot_choose_threads(cx, nm, c) / 32;
+    desc[3] = desc[4] = 0;
+    return HJB_OK;
+  }
+  JacShape sh = jacobi_default_shape(cx, nm, count);
+  if (cluster > 0 && cluster != sh.c && !jacobi_shape_for(nm, cluster, &sh))
+    return fail(HJB_EINVAL, "hjb_inner_order: no Jacobi shape with that cluster size");
+  desc[0] = 2;
+  desc[1] = nm;
+  desc[2] = sh.c;
+  desc[3] = sh.w;
+  desc[4] = sh.spw;
   return HJB_OK;
 }
 
@@ -668,6 +740,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   res->t_exchange_ms = tx;
   res->cluster_size = ctx.cluster;
   res->gram_splits = ctx.splits_used;
+  res->kernel_launches = ctx.launches;
   return HJB_OK;
 }
 
@@ -773,7 +846,10 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
   pa.uscr = ws.U.p;
   CK(ws.Gc.reserve(size_t(count) * pivot_check_elems(nmax) * (dtype == HJB_C128 ? 16 : 8)));
   pa.gchk = ws.Gc.p;
-  cudaError_t e = launch_pivot(dtype == HJB_C128, pa, cluster, st, nullptr);
+  CK(ws.R0.reserve(size_t(count) * nmax * nmax * (dtype == HJB_C128 ? 16 : 8)));
+  pa.R0g = ws.R0.p;
+  int launches = 0;
+  cudaError_t e = launch_inner(dtype == HJB_C128, pa, cluster, st, nullptr, &launches);
   if (e == cudaErrorInvalidConfiguration) return fail(HJB_EINVAL, "hjb_pivot: unsupported cluster size");
   CK(e);
   CK(cudaStreamSynchronize(st));

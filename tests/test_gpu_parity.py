@@ -78,12 +78,14 @@ def test_gram_kernel(pkg, torch, cplx, m, bmax, widths):
 
 
 def _order(pkg, cplx, bmax, count=1, cluster=0):
-    """The inner order hjb_pivot uses for this launch (oracle order string)."""
-    import ctypes as C
-
-    nm, nw = C.c_int32(), C.c_int32()
-    pkg._lib.check(pkg._lib.lib().hjb_pivot_order(1 if cplx else 0, bmax, count, cluster, C.byref(nm), C.byref(nw)))
-    return f"wblock:{nm.value}:{nw.value}"
+    """The inner order hjb_pivot uses for this launch (oracle order string):
+    the ring-of-rings Jacobi kernel ("ror:NMAX:C:W:SPW") or, with
+    HJB_PIVOT_V1=1, the round-1 warp-block order ("wblock:NMAX:WARPS")."""
+    d = np.zeros(5, np.int32)
+    pkg._lib.check(pkg._lib.lib().hjb_inner_order(1 if cplx else 0, bmax, count, cluster, d.ctypes.data))
+    if d[0] == 1:
+        return f"wblock:{d[1]}:{d[2]}"
+    return f"ror:{d[1]}:{d[2]}:{d[3]}:{d[4]}"
 
 
 def _pivot(pkg, torch, cplx, G, J, items, bmax, cluster=0, max_sweeps=30, orth_tol=None):
@@ -346,7 +348,8 @@ def test_cluster_sizes_agree(pkg, torch):
     b = 64
     J = np.array([1] * 70 + [-1] * 58, np.int8)
     items = items_array([[0, b, b, b]])
-    for cplx, clusters in ((False, (2, 4, 8)), (True, (4, 8))):
+    v1 = _order(pkg, False, b).startswith("wblock")
+    for cplx, clusters in (((False, (2, 4, 8)), (True, (4, 8))) if v1 else ((False, (4, 8)), (True, (4, 8)))):
         G = _orthonormal_blocks(rng, 256, [b, b], cplx)
         outs = [_pivot(pkg, torch, cplx, G, J, items, b, cluster=c) for c in clusters]
         orders = [_order(pkg, cplx, b, 1, c) for c in clusters]
