@@ -179,10 +179,25 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
 int hjb_plane_rotations(int32_t dtype, int32_t count, const double *a_rr, const double *a_ss,
                         const void *a_rs, const int8_t *j_rr, const int8_t *j_ss, double *out);
 
+/*
+ * The inner J-Jacobi alone (rotations.py:203-223, the ring-of-rings kernel):
+ * diagonalise the given factors R0 (device [count][ld*ld], ld =
+ * hjb_pivot_ld(bmax), column-major, item t of order ni+nj) into R_out until
+ * an inner sweep applies no rotation.  stats (device int64 [count][8]) is
+ * zeroed and receives (rotations, big, max_t bits, inner sweeps, status,
+ * fail_r, fail_s, 0); status 1 = PivotDefinitenessError(fail_r, fail_s).
+ * Test hook for the failure paths of _kernels.py:59-60, 73-74.
+ */
+int hjb_jacobi(int32_t dtype, const int32_t *items_host, int32_t count, int32_t bmax, const void *R0,
+               void *R_out, const int8_t *signs_dev, double orth_tol, double quad_tol, int32_t max_sweeps,
+               int64_t *stats, int32_t cluster, void *stream);
+
 /* Leading dimension of W / R_out used by hjb_pivot for a given bmax. */
 int hjb_pivot_ld(int32_t bmax);
-/* Debug: record per-CTA phase clocks of later hjb_pivot calls into a device
- * int64 buffer [count*cluster][8] (NULL disables). */
+/* Debug: record phase clocks of later hjb_pivot / hjb_jacobi calls into a
+ * device int64 buffer (NULL disables): per CTA [count*cluster][8] for the
+ * round-1 pivot kernel, per warp [count*C*W][8] for the Jacobi kernel
+ * (builds with -DHJB_JAC_PROF=1). */
 int hjb_pivot_set_profile(void *prof);
 /* Tuning override for the pivot kernel: threads per CTA (256/512/1024) and
  * cluster size (1..16); 0 restores the automatic choice. */

@@ -74,6 +74,8 @@ SIGNATURES = {
                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "hjb_pivot_ld": (C.c_int, [C.c_int32]),
+    "hjb_jacobi": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                             C.c_double, C.c_double, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "hjb_plane_rotations": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p]),
     "hjb_pivot_set_profile": (C.c_int, [C.c_void_p]),

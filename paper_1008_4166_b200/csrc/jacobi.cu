@@ -45,6 +45,17 @@
 
 namespace cg = cooperative_groups;
 
+// per-warp phase clocks (tools/jac_bench.py); compiled out unless
+// -DHJB_JAC_PROF=1 (a separate profiling build of the library)
+#ifndef HJB_JAC_PROF
+#define HJB_JAC_PROF 0
+#endif
+#if HJB_JAC_PROF
+#define JCLK() clock64()
+#else
+#define JCLK() 0LL
+#endif
+
 namespace hjb {
 
 namespace {
@@ -92,6 +103,18 @@ __device__ __forceinline__ void jb_wait(uint64_t *bar, unsigned parity) {
       " @!p bra JB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void jb_wait_cta(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "JB_WAITC_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra JB_WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void jb_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ uint32_t jb_mapa(uint32_t addr, int rank) {
   uint32_t r;
@@ -214,8 +237,14 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   for (int c = tid; c < N; c += Cfg::NT)
     Jv[c] = c < ni ? a.signs[it.oi + c] : (c < Nq ? a.signs[it.oj + (c - ni)] : 1);
   if (tid < 2 * W) {
-    jb_init(&bars[(tid >> 1) * 4 + (tid & 1)], 1);      // full[dir]: the receiver's expect_tx arrival
-    jb_init(&bars[(tid >> 1) * 4 + 2 + (tid & 1)], 1);  // empty[dir]: the receiver's remote arrival
+    // full[dir] of warp w: the receiver's own arrival (+ expect_tx when the
+    // sender is in another CTA, + the sender's arrival when it is local);
+    // dir 0 receives from q+1 (remote for the last warp), dir 1 from q-1
+    // (remote for warp 0); empty[dir]: the receiver's arrival
+    const int w = tid >> 1, dr = tid & 1;
+    const bool remote = C > 1 && (dr == 0 ? w == W - 1 : w == 0);
+    jb_init(&bars[w * 4 + dr], remote ? 1 : 2);
+    jb_init(&bars[w * 4 + 2 + dr], 1);
   }
   if (tid == 0) {
     s_cnt[0] = s_cnt[1] = 0;
@@ -247,10 +276,13 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   long long nrot_total = 0, big_total = 0;
   int sweeps = 0, status = PV_OK;
   int gdir[2] = {0, 0};  // messages sent/received per direction (equal in every worker)
+  long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // round, empty wait, send, full wait, receive, sweep end, rounds, t0
+  pf[7] = JCLK();
 
   // -------------------------------------------------------------- one round
   // pairs (slot A(k), slot B(k)), k < SPW, of this warp; A plays r, B plays s
   auto round = [&](auto pa, auto pb) {
+    const long long r0 = JCLK();
     T dp[SPW];
     sfor<SPW>([&](auto k) {
       constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
@@ -299,14 +331,13 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     p.sp = S<T>::zero();
     p.hs = 0.0;
     p.cs = 1.0;
-    double te_n = 0.0, te_d = 1.0, te_h = 0.0;
+    double te_n = 0.0, te_h = 0.0;
     if (__any_sync(0xffffffffu, rot)) {
       if (rot) {
         const RotCoef<T> r = rot_coef<T>(acc, dr, ds, sr == ss, otol2);
         if (r.code == 1) {
           p = r;
-          te_n = r.num * r.eta;
-          te_d = r.den;
+          te_n = r.num * r.eta / r.den;  // t * eta (_kernels.py:80-81)
           te_h = r.hyp;
           if ((lane & (GS - 1)) == 0) {
             ++my_cnt;
@@ -331,16 +362,18 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
           pk.sp = shfl_idx(p.sp, src);
           pk.hs = __shfl_sync(0xffffffffu, p.hs, src);
           pk.cs = __shfl_sync(0xffffffffu, p.cs, src);
-          const double tn = __shfl_sync(0xffffffffu, te_n, src);
-          const double td = __shfl_sync(0xffffffffu, te_d, src);
+          const double te = __shfl_sync(0xffffffffu, te_n, src);
           const double th = __shfl_sync(0xffffffffu, te_h, src);
 #pragma unroll
           for (int u = 0; u < RPL; ++u) rot_fold<T>(V[u][A], V[u][B], pk);
-          const double te = tn / td;  // t * eta (_kernels.py:80-81)
           D[A] = fma(th, te, D[A]);
           D[B] = D[B] + te;
         }
       });
+    }
+    if (HJB_JAC_PROF) {
+      pf[0] += JCLK() - r0;
+      pf[6] += 1;
     }
   };
 
@@ -361,7 +394,10 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   };
 
   // ---------------------------------------------------------- the exchange
-  // strategies.py:69-72: odd sweeps send to q-1 and receive from q+1
+  // strategies.py:69-72: odd sweeps send to q-1 and receive from q+1.  Links
+  // inside a CTA use plain shared-memory stores and a counted arrival; the
+  // two links that cross a CTA boundary use st.async into the neighbour's
+  // shared memory (DSMEM) completing on its barrier's transaction count.
   auto exchange = [&](int nsweep) {
     const int old_i = sp.ib, old_j = sp.jb;
     const int snd = sp.step(NBL);
@@ -370,30 +406,45 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     const int d = (nsweep & 1) ? 0 : 1;
     const int dst = (nsweep & 1) ? (q + Q - 1) % Q : (q + 1) % Q;
     const int srcw = (nsweep & 1) ? (q + 1) % Q : (q + Q - 1) % Q;
+    const int dc = dst / W, dw = dst % W, sc = srcw / W, sw = srcw % W;
+    const bool rsend = C > 1 && dc != crank, rrecv = C > 1 && sc != crank;
     const int g = gdir[d]++;
     uint64_t *full = &bars[warp * 4 + d];
     uint64_t *empty = &bars[warp * 4 + 2 + d];
     // send: wait until the receiver has consumed this link's previous message
-    if (g > 0) jb_wait(empty, (g - 1) & 1);
+    const long long x0 = JCLK();
+    if (g > 0) {
+      if (rsend) jb_wait(empty, (g - 1) & 1);
+      else jb_wait_cta(empty, (g - 1) & 1);
+    }
+    const long long x1 = JCLK();
     {
-      const int dc = dst / W, dw = dst % W;
       T *box = inbox + (size_t(dw) * 2 + d) * MSG;
-      const uint32_t rbox = jb_mapa(smem_u32(box), dc);
-      const uint32_t rbar = jb_mapa(smem_u32(&bars[dw * 4 + d]), dc);
+      double dv = 0.0;
       sfor<SPW>([&](auto k) {
-        constexpr int K = decltype(k)::value;
-#pragma unroll
-        for (int u = 0; u < RPL; ++u) {
-          const T v = send_i ? V[u][K] : V[u][SPW + K];
-          jb_st_async(rbox + uint32_t((K * N + lane + 32 * u) * sizeof(T)), v, rbar);
-        }
+        if (lane == decltype(k)::value) dv = send_i ? D[decltype(k)::value] : D[SPW + decltype(k)::value];
       });
-      if (lane < SPW) {
-        double dv = 0.0;
+      if (rsend) {
+        const uint32_t rbox = jb_mapa(smem_u32(box), dc);
+        const uint32_t rbar = jb_mapa(smem_u32(&bars[dw * 4 + d]), dc);
         sfor<SPW>([&](auto k) {
-          if (lane == decltype(k)::value) dv = send_i ? D[decltype(k)::value] : D[SPW + decltype(k)::value];
+          constexpr int K = decltype(k)::value;
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) {
+            const T v = send_i ? V[u][K] : V[u][SPW + K];
+            jb_st_async(rbox + uint32_t((K * N + lane + 32 * u) * sizeof(T)), v, rbar);
+          }
         });
-        jb_st_async(rbox + uint32_t((SPW * N + lane) * sizeof(T)), scale(S<T>::one(), dv), rbar);
+        if (lane < SPW) jb_st_async(rbox + uint32_t((SPW * N + lane) * sizeof(T)), scale(S<T>::one(), dv), rbar);
+      } else {
+        sfor<SPW>([&](auto k) {
+          constexpr int K = decltype(k)::value;
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) box[K * N + lane + 32 * u] = send_i ? V[u][K] : V[u][SPW + K];
+        });
+        if (lane < SPW) box[SPW * N + lane] = scale(S<T>::one(), dv);
+        __syncwarp();
+        if (lane == 0) jb_arrive(&bars[dw * 4 + d]);
       }
     }
     // receive into the vacated slots
@@ -405,8 +456,13 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
         D[K] = D[SPW + K];
       });
     }
-    if (lane == 0) jb_arrive_expect(full, Cfg::MSG_BYTES);
-    jb_wait(full, g & 1);
+    if (lane == 0) {
+      if (rrecv) jb_arrive_expect(full, Cfg::MSG_BYTES);
+      else jb_arrive(full);
+    }
+    const long long x2 = JCLK();
+    jb_wait_cta(full, g & 1);
+    const long long x3 = JCLK();
     const T *box = inbox + (size_t(warp) * 2 + d) * MSG;
     const bool into_i = send_i && !swap;
     sfor<SPW>([&](auto k) {
@@ -421,8 +477,15 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     });
     __syncwarp();
     if (lane == 0) {
-      const int sc = srcw / W, sw = srcw % W;
-      jb_arrive_remote(jb_mapa(smem_u32(&bars[sw * 4 + 2 + d]), sc));
+      if (rrecv) jb_arrive_remote(jb_mapa(smem_u32(&bars[sw * 4 + 2 + d]), sc));
+      else jb_arrive(&bars[sw * 4 + 2 + d]);
+    }
+    if (HJB_JAC_PROF) {
+      const long long x4 = JCLK();
+      pf[1] += x1 - x0;
+      pf[2] += x2 - x1;
+      pf[3] += x3 - x2;
+      pf[4] += x4 - x3;
     }
   };
 
@@ -454,6 +517,7 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     }
     // ---- sweep end: cluster-wide rotation count (parallel.py:239-244 at the
     // inner level, rotations.py:220-222) ----
+    const long long e0 = JCLK();
     const int par = sw & 1;
     {
       const int wc = __reduce_add_sync(0xffffffffu, my_cnt);
@@ -485,6 +549,7 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     }
     big_total += big;
     nrot_total += tot;
+    if (HJB_JAC_PROF) pf[5] += JCLK() - e0;
     if (fl != INT_MAX) {
       status = PV_INDEFINITE;
       my_fail = fl;
@@ -520,6 +585,11 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
       st[ST_FS] = status == PV_INDEFINITE ? my_fail % 4096 : -1;
     }
   }
+  if (HJB_JAC_PROF && a.prof && lane == 0) {
+    long long *o = a.prof + (int64_t(blockIdx.x) * W + warp) * 8;
+    pf[7] = JCLK() - pf[7];
+    for (int k = 0; k < 8; ++k) o[k] = pf[k];
+  }
   jb_cluster_sync<C>();  // peers' shared memory stays alive until read
 }
 
@@ -528,9 +598,8 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
 template <typename T, int N, int C, int W, int SPW>
 static cudaError_t launch_jacobi_t(const JacobiArgs &a, cudaStream_t st) {
   using Cfg = JacCfg<T, N, C, W, SPW>;
-  // two CTAs per SM when the register-resident columns allow it
-  constexpr int REGS = 2 * Cfg::RPL * Cfg::CPW * int(sizeof(T) / 8);
-  constexpr int MINB = REGS <= 64 ? 2 : 1;
+  // two CTAs per SM for 4-warp CTAs (255 registers per thread either way)
+  constexpr int MINB = Cfg::NT <= 128 ? 2 : 1;
   auto k = jacobi_kernel<T, N, C, W, SPW, MINB>;
   static DeviceFlags attr_flags;
   bool *attr = attr_flags.here();
@@ -593,10 +662,18 @@ bool jacobi_shape_for(int nmax, int c, JacShape *out) {
   return false;
 }
 
+// register-resident columns per lane (RPL x 2 SPW elements) that fit without
+// spilling: 64 doubles
+template <typename T, int N, int SPW>
+constexpr bool jac_shape_ok() {
+  return (N / 32) * 2 * SPW * int(sizeof(T) / 8) <= 64;
+}
+
 template <typename T>
 static cudaError_t dispatch_jacobi(const JacobiArgs &a, JacShape s, cudaStream_t st) {
 #define HJB_JAC_CASE(N_, C_, W_, S_)                                              \
-  if (a.nmax == N_ && s.c == C_ && s.w == W_ && s.spw == S_) return launch_jacobi_t<T, N_, C_, W_, S_>(a, st);
+  if constexpr (jac_shape_ok<T, N_, S_>())                                         \
+    if (a.nmax == N_ && s.c == C_ && s.w == W_ && s.spw == S_) return launch_jacobi_t<T, N_, C_, W_, S_>(a, st);
   HJB_JAC_SHAPES(HJB_JAC_CASE)
 #undef HJB_JAC_CASE
   return cudaErrorInvalidConfiguration;

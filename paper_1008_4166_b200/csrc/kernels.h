@@ -70,6 +70,7 @@ struct JacobiArgs {
   double orth_tol, quad_tol;
   int max_sweeps;
   int64_t *stats;        // [count][ST_N]: status/fallback in, counters out
+  long long *prof;       // optional per-warp phase clocks [count*C*W][8] (HJB_JAC_PROF builds)
 };
 struct JacShape {
   int c, w, spw;  // cluster size, warps per CTA, pairs per warp (nmax = 2 c w spw)

@@ -209,6 +209,7 @@ __global__ void plane_rotation_kernel(int count, const double *arr, const double
   const double ri = q > 0.0 ? rsqrt(q) : 0.0;
   const double sa = re(a) >= 0.0 ? 1.0 : -1.0;
   T ph = phase_mul(a, sa * ri);
+  if constexpr (!S<T>::cx) ph = 1.0;  // a / eta is exactly 1 for real a (_kernels.py:61-62)
   o[0] = p.code;
   o[1] = p.code == 1 ? p.cs : 1.0;
   o[2] = p.code == 1 ? p.hs * p.hyp : 0.0;  // sn (hs = hyp * sn)

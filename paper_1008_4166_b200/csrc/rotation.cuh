@@ -33,9 +33,16 @@ __device__ __forceinline__ RotCoef<T> rot_coef(T a, double dr, double ds, bool s
   const double q = abs2(a);
   const double dd = dr * ds;
   const double q4 = 4.0 * q;
-  const double ri = rsqrt(q);
   const double sa = re(a) >= 0.0 ? 1.0 : -1.0;
-  const double aa = q * ri;
+  // |a| and the phase a/eta: for real a the phase is exactly 1 (a / eta with
+  // eta = a, _kernels.py:61-62), so no reciprocal square root is needed
+  double ri = 0.0, aa;
+  if constexpr (S<T>::cx) {
+    ri = rsqrt(q);
+    aa = q * ri;
+  } else {
+    aa = fabs(re(a));
+  }
   const double x = same ? ds - dr : dr + ds;
   const double sq4 = same ? q4 : -q4;
   const double disc = fma(x, x, sq4);
@@ -48,11 +55,16 @@ __device__ __forceinline__ RotCoef<T> rot_coef(T a, double dr, double ds, bool s
   p.code = skip ? 0 : (bad ? -1 : 1);
   p.hyp = same ? -1.0 : 1.0;
   const double cs = den * r, sn = num * r;
-  const T ph = phase_mul(a, sa * ri);
   p.cs = cs;
   p.hs = p.hyp * sn;
-  p.cp = phase_mul(ph, cs);
-  p.sp = phase_mul(ph, sn);
+  if constexpr (S<T>::cx) {
+    const T ph = phase_mul(a, sa * ri);
+    p.cp = phase_mul(ph, cs);
+    p.sp = phase_mul(ph, sn);
+  } else {
+    p.cp = cs;
+    p.sp = sn;
+  }
   p.num = num;
   p.den = den;
   p.eta = sa * aa;

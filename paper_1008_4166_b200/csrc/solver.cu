@@ -154,6 +154,8 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
     ++*launches;
     return launch_pivot(cx, pa, cluster_req, st, cluster_used);
   }
+  long long *prof = pa.prof;  // phase clocks are the Jacobi kernel's
+  pa.prof = nullptr;
   pa.mode = PV_PROLOGUE;
   cudaError_t e = launch_pivot(cx, pa, 0, st, nullptr);
   if (e != cudaSuccess) return e;
@@ -169,6 +171,7 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   j.quad_tol = pa.quad_tol;
   j.max_sweeps = pa.max_sweeps;
   j.stats = pa.stats;
+  j.prof = prof;
   JacShape sh = jacobi_default_shape(cx, pa.nmax, pa.count);
   if (cluster_req > 0 && cluster_req != sh.c && !jacobi_shape_for(pa.nmax, cluster_req, &sh))
     return cudaErrorInvalidConfiguration;  // no instantiated shape with that cluster size
@@ -852,6 +855,42 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
   cudaError_t e = launch_inner(dtype == HJB_C128, pa, cluster, st, nullptr, &launches);
   if (e == cudaErrorInvalidConfiguration) return fail(HJB_EINVAL, "hjb_pivot: unsupported cluster size");
   CK(e);
+  CK(cudaStreamSynchronize(st));
+  return HJB_OK;
+}
+
+int hjb_jacobi(int32_t dtype, const int32_t *items_host, int32_t count, int32_t bmax, const void *R0, void *R_out,
+               const int8_t *signs_dev, double orth_tol, double quad_tol, int32_t max_sweeps, int64_t *stats,
+               int32_t cluster, void *stream) {
+  if (count < 1 || bmax < 1 || !R0 || !R_out || !stats || !signs_dev || max_sweeps < 1)
+    return fail(HJB_EINVAL, "hjb_jacobi: bad arguments");
+  const int nmax = pivot_nmax(bmax);
+  if (nmax < 0) return fail(HJB_EINVAL, "hjb_jacobi: block width too large");
+  const bool cx = dtype == HJB_C128;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  Workspace &ws = g_ws[dev];
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = upload_items(ws, items_host, count, st)) return rc;
+  CK(cudaMemsetAsync(stats, 0, size_t(count) * ST_N * sizeof(int64_t), st));
+  JacobiArgs j{};
+  j.items = static_cast<const Item *>(ws.items.p);
+  j.count = count;
+  j.nmax = nmax;
+  j.ld = nmax;
+  j.R0 = R0;
+  j.Rout = R_out;
+  j.signs = signs_dev;
+  j.orth_tol = orth_tol;
+  j.quad_tol = quad_tol;
+  j.max_sweeps = max_sweeps;
+  j.stats = stats;
+  j.prof = g_pivot_prof;
+  JacShape sh = jacobi_default_shape(cx, nmax, count);
+  if (cluster > 0 && cluster != sh.c && !jacobi_shape_for(nmax, cluster, &sh))
+    return fail(HJB_EINVAL, "hjb_jacobi: no Jacobi shape with that cluster size");
+  CK(launch_jacobi(cx, j, sh, st));
   CK(cudaStreamSynchronize(st));
   return HJB_OK;
 }
