@@ -50,6 +50,9 @@ namespace cg = cooperative_groups;
 #ifndef HJB_JAC_PROF
 #define HJB_JAC_PROF 0
 #endif
+#ifndef HJB_JAC_FUSE  // 1: gather-first + fused next-round dots (slower on B200: register pressure)
+#define HJB_JAC_FUSE 0
+#endif
 #if HJB_JAC_PROF
 #define JCLK() clock64()
 #else
@@ -275,15 +278,28 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   double my_maxt = 0.0;
   long long nrot_total = 0, big_total = 0;
   int sweeps = 0, status = PV_OK;
-  int gdir[2] = {0, 0};  // messages sent/received per direction (equal in every worker)
   long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // round, empty wait, send, full wait, receive, sweep end, rounds, t0
   pf[7] = JCLK();
 
+  // per-slot column state: J sign and "real column" flag (ids >= Nq are padding)
+  int sg[CPW];
+  bool live[CPW];
+  auto refresh_slot = [&](int c) {
+    const int col = col_of(c);
+    sg[c] = Jv[col];
+    live[c] = col < Nq;
+  };
+  sfor<CPW>([&](auto c) { refresh_slot(c); });
+
   // -------------------------------------------------------------- one round
-  // pairs (slot A(k), slot B(k)), k < SPW, of this warp; A plays r, B plays s
-  auto round = [&](auto pa, auto pb) {
-    const long long r0 = JCLK();
-    T dp[SPW];
+  // The round's SPW pairs (slot A(k), slot B(k)); A plays r, B plays s.  The
+  // dot partials are reduce-scattered over the warp (lane group kk owns pair
+  // kk), each group derives its pair's rotation, the parameters of all pairs
+  // are gathered by shuffles, and the rotations are applied row by row fused
+  // with the next round's dot partials (HJB_JAC_FUSE; when the next pairing is
+  // in the same step, NEXT).
+  T dp[SPW];
+  auto dots = [&](auto pa, auto pb) {
     sfor<SPW>([&](auto k) {
       constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
       T d0 = S<T>::zero(), d1 = S<T>::zero();
@@ -294,7 +310,11 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
       }
       dp[k] = add(d0, d1);
     });
-    // butterfly reduce-scatter: lane keeps pair kk = lane >> (5 - S)
+  };
+  auto round = [&](auto pa, auto pb, auto na, auto nb, auto has_next) {
+    constexpr bool NEXT = HJB_JAC_FUSE && decltype(has_next)::value;
+    const long long r0 = JCLK();
+    // butterfly reduce-scatter: lane keeps pair kk = lane >> (5 - LS)
 #pragma unroll
     for (int j = 0; j < LS; ++j) {
       const int dist = 16 >> j;
@@ -311,47 +331,88 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
 #pragma unroll
     for (int dist = 16 >> LS; dist >= 1; dist >>= 1) acc = add(acc, shfl_xor(acc, dist));
     const int kk = lane >> (5 - LS);
-    // this lane's pair: D values, signs, column ids
     double dr = 0.0, ds = 0.0;
-    int sr = 1, ss = 1, cr = 0, cs = 0;
+    int sr = 1, ss = 1, ar = 0, as = 0;
+    bool lv = false;
     sfor<SPW>([&](auto k) {
       constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
       if (kk == k) {
         dr = D[A];
         ds = D[B];
-        cr = col_of(A);
-        cs = col_of(B);
+        sr = sg[A];
+        ss = sg[B];
+        lv = live[A] && live[B];
+        ar = A;
+        as = B;
       }
     });
-    sr = Jv[cr];
-    ss = Jv[cs];
-    bool rot = cr < Nq && cs < Nq && !(abs2(acc) <= otol2 * (dr * ds));  // _kernels.py:57
+    bool rot = lv && !(abs2(acc) <= otol2 * (dr * ds));  // _kernels.py:57
     RotCoef<T> p;
     p.cp = S<T>::one();
     p.sp = S<T>::zero();
     p.hs = 0.0;
     p.cs = 1.0;
     double te_n = 0.0, te_h = 0.0;
-    if (__any_sync(0xffffffffu, rot)) {
-      if (rot) {
-        const RotCoef<T> r = rot_coef<T>(acc, dr, ds, sr == ss, otol2);
-        if (r.code == 1) {
-          p = r;
-          te_n = r.num * r.eta / r.den;  // t * eta (_kernels.py:80-81)
-          te_h = r.hyp;
-          if ((lane & (GS - 1)) == 0) {
-            ++my_cnt;
-            const double t = fabs(r.num) / r.den;
-            my_big += fabs(r.num) > qtol * r.den;  // |t| > quad_tol
-            my_maxt = fmax(my_maxt, t);
-          }
-        } else {
-          rot = false;
-          if (r.code < 0 && (lane & (GS - 1)) == 0) my_fail = min(my_fail, min(cr, cs) * 4096 + max(cr, cs));
+    const bool any = __any_sync(0xffffffffu, rot);
+    if (any && rot) {
+      const RotCoef<T> r = rot_coef<T>(acc, dr, ds, sr == ss, otol2);
+      if (r.code == 1) {
+        p = r;
+        te_n = r.num * r.eta / r.den;  // t * eta (_kernels.py:80-81)
+        te_h = r.hyp;
+        if ((lane & (GS - 1)) == 0) {
+          ++my_cnt;
+          my_big += fabs(r.num) > qtol * r.den;  // |t| > quad_tol
+          my_maxt = fmax(my_maxt, fabs(r.num) / r.den);
+        }
+      } else {
+        rot = false;
+        if (r.code < 0 && (lane & (GS - 1)) == 0) {
+          const int cr = col_of(ar), cs = col_of(as);
+          my_fail = min(my_fail, min(cr, cs) * 4096 + max(cr, cs));
         }
       }
-      // every lane applies every pair of the warp: parameters of pair k from
-      // the first lane of its group
+    }
+#if HJB_JAC_FUSE
+    // gather every pair's parameters (first lane of its group), then one
+    // fused pass over the rows
+    RotCoef<T> pk[SPW];
+    bool rk[SPW];
+    if (any) {
+      sfor<SPW>([&](auto k) {
+        constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
+        const int src = k * GS;
+        rk[k] = __shfl_sync(0xffffffffu, rot, src);
+        pk[k].cp = shfl_idx(p.cp, src);
+        pk[k].sp = shfl_idx(p.sp, src);
+        pk[k].hs = __shfl_sync(0xffffffffu, p.hs, src);
+        pk[k].cs = __shfl_sync(0xffffffffu, p.cs, src);
+        const double te = __shfl_sync(0xffffffffu, te_n, src);
+        const double th = __shfl_sync(0xffffffffu, te_h, src);
+        if (rk[k]) {
+          D[A] = fma(th, te, D[A]);
+          D[B] = D[B] + te;
+        }
+      });
+    }
+    if constexpr (NEXT) sfor<SPW>([&](auto k) { dp[k] = S<T>::zero(); });
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      if (any) {
+        sfor<SPW>([&](auto k) {
+          constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
+          if (rk[k]) rot_fold<T>(V[u][A], V[u][B], pk[k]);
+        });
+      }
+      if constexpr (NEXT) {
+        sfor<SPW>([&](auto k) {
+          constexpr int A = decltype(na(k))::value, B = decltype(nb(k))::value;
+          dp[k] = cfma(V[u][A], V[u][B], dp[k]);
+        });
+      }
+    }
+#else
+    if (any) {
       sfor<SPW>([&](auto k) {
         constexpr int A = decltype(pa(k))::value, B = decltype(pb(k))::value;
         const int src = k * GS;
@@ -371,25 +432,43 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
         }
       });
     }
+#endif
+    if constexpr (!NEXT) {
+      if constexpr (decltype(has_next)::value) dots(na, nb);
+    }
     if (HJB_JAC_PROF) {
       pf[0] += JCLK() - r0;
       pf[6] += 1;
     }
   };
+  using BT = std::integral_constant<bool, true>;
+  using BF = std::integral_constant<bool, false>;
 
   // phase A: all pairs of the warp's 2 SPW columns; phase B: i x j
   auto phase_a = [&]() {
+    dots([](auto k) { return std::integral_constant<int, PhaseA<SPW>::a(0, decltype(k)::value)>{}; },
+         [](auto k) { return std::integral_constant<int, PhaseA<SPW>::b(0, decltype(k)::value)>{}; });
     sfor<CPW - 1>([&](auto r) {
       constexpr int R = decltype(r)::value;
-      round([](auto k) { return std::integral_constant<int, PhaseA<SPW>::a(R, decltype(k)::value)>{}; },
-            [](auto k) { return std::integral_constant<int, PhaseA<SPW>::b(R, decltype(k)::value)>{}; });
+      constexpr int R1 = R + 1 < CPW - 1 ? R + 1 : R;
+      auto pa = [](auto k) { return std::integral_constant<int, PhaseA<SPW>::a(R, decltype(k)::value)>{}; };
+      auto pb = [](auto k) { return std::integral_constant<int, PhaseA<SPW>::b(R, decltype(k)::value)>{}; };
+      auto na = [](auto k) { return std::integral_constant<int, PhaseA<SPW>::a(R1, decltype(k)::value)>{}; };
+      auto nb = [](auto k) { return std::integral_constant<int, PhaseA<SPW>::b(R1, decltype(k)::value)>{}; };
+      if constexpr (R + 1 < CPW - 1) round(pa, pb, na, nb, BT{});
+      else round(pa, pb, na, nb, BF{});
     });
   };
   auto phase_b = [&]() {
+    dots([](auto k) { return std::integral_constant<int, decltype(k)::value>{}; },
+         [](auto k) { return std::integral_constant<int, SPW + decltype(k)::value>{}; });
     sfor<SPW>([&](auto r) {
       constexpr int R = decltype(r)::value;
-      round([](auto k) { return std::integral_constant<int, decltype(k)::value>{}; },
-            [](auto k) { return std::integral_constant<int, SPW + (decltype(k)::value + R) % SPW>{}; });
+      auto pa = [](auto k) { return std::integral_constant<int, decltype(k)::value>{}; };
+      auto pb = [](auto k) { return std::integral_constant<int, SPW + (decltype(k)::value + R) % SPW>{}; };
+      auto nb = [](auto k) { return std::integral_constant<int, SPW + (decltype(k)::value + R + 1) % SPW>{}; };
+      if constexpr (R + 1 < SPW) round(pa, pb, pa, nb, BT{});
+      else round(pa, pb, pa, nb, BF{});
     });
   };
 
@@ -398,6 +477,7 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   // inside a CTA use plain shared-memory stores and a counted arrival; the
   // two links that cross a CTA boundary use st.async into the neighbour's
   // shared memory (DSMEM) completing on its barrier's transaction count.
+  int g_dn = 0, g_up = 0;  // messages per direction (equal in every worker)
   auto exchange = [&](int nsweep) {
     const int old_i = sp.ib, old_j = sp.jb;
     const int snd = sp.step(NBL);
@@ -408,7 +488,7 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     const int srcw = (nsweep & 1) ? (q + 1) % Q : (q + Q - 1) % Q;
     const int dc = dst / W, dw = dst % W, sc = srcw / W, sw = srcw % W;
     const bool rsend = C > 1 && dc != crank, rrecv = C > 1 && sc != crank;
-    const int g = gdir[d]++;
+    const int g = d == 0 ? g_dn++ : g_up++;
     uint64_t *full = &bars[warp * 4 + d];
     uint64_t *empty = &bars[warp * 4 + 2 + d];
     // send: wait until the receiver has consumed this link's previous message
@@ -418,35 +498,36 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
       else jb_wait_cta(empty, (g - 1) & 1);
     }
     const long long x1 = JCLK();
-    {
-      T *box = inbox + (size_t(dw) * 2 + d) * MSG;
+    T *box_out = inbox + (size_t(dw) * 2 + d) * MSG;
+    auto send = [&](auto base) {
+      constexpr int B0 = decltype(base)::value;
       double dv = 0.0;
       sfor<SPW>([&](auto k) {
-        if (lane == decltype(k)::value) dv = send_i ? D[decltype(k)::value] : D[SPW + decltype(k)::value];
+        if (lane == decltype(k)::value) dv = D[B0 + decltype(k)::value];
       });
       if (rsend) {
-        const uint32_t rbox = jb_mapa(smem_u32(box), dc);
+        const uint32_t rbox = jb_mapa(smem_u32(box_out), dc);
         const uint32_t rbar = jb_mapa(smem_u32(&bars[dw * 4 + d]), dc);
         sfor<SPW>([&](auto k) {
           constexpr int K = decltype(k)::value;
 #pragma unroll
-          for (int u = 0; u < RPL; ++u) {
-            const T v = send_i ? V[u][K] : V[u][SPW + K];
-            jb_st_async(rbox + uint32_t((K * N + lane + 32 * u) * sizeof(T)), v, rbar);
-          }
+          for (int u = 0; u < RPL; ++u)
+            jb_st_async(rbox + uint32_t((K * N + lane + 32 * u) * sizeof(T)), V[u][B0 + K], rbar);
         });
         if (lane < SPW) jb_st_async(rbox + uint32_t((SPW * N + lane) * sizeof(T)), scale(S<T>::one(), dv), rbar);
       } else {
         sfor<SPW>([&](auto k) {
           constexpr int K = decltype(k)::value;
 #pragma unroll
-          for (int u = 0; u < RPL; ++u) box[K * N + lane + 32 * u] = send_i ? V[u][K] : V[u][SPW + K];
+          for (int u = 0; u < RPL; ++u) box_out[K * N + lane + 32 * u] = V[u][B0 + K];
         });
-        if (lane < SPW) box[SPW * N + lane] = scale(S<T>::one(), dv);
+        if (lane < SPW) box_out[SPW * N + lane] = scale(S<T>::one(), dv);
         __syncwarp();
         if (lane == 0) jb_arrive(&bars[dw * 4 + d]);
       }
-    }
+    };
+    if (send_i) send(std::integral_constant<int, 0>{});
+    else send(std::integral_constant<int, SPW>{});
     // receive into the vacated slots
     if (swap) {
       sfor<SPW>([&](auto k) {
@@ -464,22 +545,23 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     jb_wait_cta(full, g & 1);
     const long long x3 = JCLK();
     const T *box = inbox + (size_t(warp) * 2 + d) * MSG;
-    const bool into_i = send_i && !swap;
-    sfor<SPW>([&](auto k) {
-      constexpr int K = decltype(k)::value;
+    auto recv = [&](auto base) {
+      constexpr int B0 = decltype(base)::value;
+      sfor<SPW>([&](auto k) {
+        constexpr int K = decltype(k)::value;
 #pragma unroll
-      for (int u = 0; u < RPL; ++u) {
-        const T v = box[K * N + lane + 32 * u];
-        if (into_i) V[u][K] = v; else V[u][SPW + K] = v;
-      }
-      const double dv = re(box[SPW * N + K]);
-      if (into_i) D[K] = dv; else D[SPW + K] = dv;
-    });
+        for (int u = 0; u < RPL; ++u) V[u][B0 + K] = box[K * N + lane + 32 * u];
+        D[B0 + K] = re(box[SPW * N + K]);
+      });
+    };
+    if (send_i && !swap) recv(std::integral_constant<int, 0>{});
+    else recv(std::integral_constant<int, SPW>{});
     __syncwarp();
     if (lane == 0) {
       if (rrecv) jb_arrive_remote(jb_mapa(smem_u32(&bars[sw * 4 + 2 + d]), sc));
       else jb_arrive(&bars[sw * 4 + 2 + d]);
     }
+    sfor<CPW>([&](auto c) { refresh_slot(c); });
     if (HJB_JAC_PROF) {
       const long long x4 = JCLK();
       pf[1] += x1 - x0;
@@ -640,13 +722,13 @@ JacShape jacobi_default_shape(bool cx, int nmax, int count) {
     if (const char *e = std::getenv("HJB_JAC_SHAPE")) sscanf(e, "%d,%d,%d", &ov_c, &ov_w, &ov_s);
   }
   if (ov_c > 0 && 2 * ov_c * ov_w * ov_s == nmax) return JacShape{ov_c, ov_w, ov_s};
-  (void)cx;
   (void)count;
+  // measured on B200 (tools/jac_bench.py, profiles/r2_jacobi_shapes.jsonl)
   switch (nmax) {
     case 32: return JacShape{1, 4, 4};
-    case 64: return JacShape{2, 4, 4};
+    case 64: return JacShape{4, 4, 2};
     case 128: return JacShape{8, 4, 2};
-    case 256: return JacShape{8, 8, 2};
+    case 256: return cx ? JacShape{16, 4, 2} : JacShape{4, 8, 4};
   }
   return JacShape{0, 0, 0};
 }

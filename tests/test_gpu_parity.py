@@ -486,17 +486,18 @@ def test_rank_deficient_factor(pkg, rng):
 @pytest.mark.parametrize("cplx", [False, True])
 def test_jacobi_indefinite_pivot_reports_r_s(pkg, torch, cplx):
     """The Jacobi kernel's failure path (_kernels.py:59-60 -> jacobi_cycle's
-    PivotDefinitenessError(r, s), rotations.py:198-199): a factor whose
-    columns 5 and 37 are equal has |a|^2 = d_r d_s exactly, so the pair fails
-    whatever the inner order; status 1 with (r, s) = (5, 37)."""
+    PivotDefinitenessError(r, s), rotations.py:198-199): in a factor whose
+    columns are mutually orthogonal except columns 5 and 37, which are equal,
+    no other pair rotates and (5, 37) has |a|^2 = d_r d_s exactly, whatever
+    the inner order; status 1 with (r, s) = (5, 37)."""
     L = pkg._lib.lib()
     b = 32
     nmax = L.hjb_pivot_ld(b)
     N = 2 * b
     rng = np.random.default_rng(3)
-    R = np.triu(rng.standard_normal((N, N))) + 4 * np.eye(N)
+    R = np.diag(rng.uniform(1.0, 4.0, N)).astype(np.complex128 if cplx else np.float64)
     if cplx:
-        R = R + 1j * np.triu(rng.standard_normal((N, N)), 1)
+        R = R * np.exp(1j * rng.uniform(0, 2 * np.pi, N))[None, :]
     R[:, 37] = R[:, 5]
     R0 = np.zeros((nmax, nmax), R.dtype)
     R0[:N, :N] = R
