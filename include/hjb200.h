@@ -115,6 +115,10 @@ int hjb_solve(const hjb_problem *prob, hjb_result *res);
  */
 int hjb_schedule(int32_t strategy, int32_t p, int32_t sweeps, int32_t *layouts,
                  int32_t *plans);
+/* The uniform block partition of the ring (blocking.py:63-68, parallel.py:
+ * 266): nbl blocks of near-equal width, wider ones first; offsets: int64
+ * [nbl + 1] (offsets[nbl] = n).  Host-only. */
+int hjb_partition(int64_t n, int32_t nbl, int64_t *offsets);
 /* steps_per_sweep (strategies.py:27-28). */
 int hjb_steps_per_sweep(int32_t strategy, int32_t p);
 

@@ -64,6 +64,7 @@ SIGNATURES = {
     "hjb_solve": (C.c_int, [C.POINTER(Problem), C.POINTER(Result)]),
     "hjb_schedule": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "hjb_steps_per_sweep": (C.c_int, [C.c_int32, C.c_int32]),
+    "hjb_partition": (C.c_int, [C.c_int64, C.c_int32, C.c_void_p]),
     "hjb_extract": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "hjb_orthogonality": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,

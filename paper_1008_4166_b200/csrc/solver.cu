@@ -347,6 +347,14 @@ int hjb_exchange_plan(int32_t strategy, int32_t p, int32_t world, int32_t rank, 
   return HJB_OK;
 }
 
+int hjb_partition(int64_t n, int32_t nbl, int64_t *offsets) {
+  if (nbl < 1 || n < nbl || !offsets) return fail(HJB_EINVAL, "hjb_partition: need 1 <= nbl <= n");
+  const Partition P = uniform_partition(n, nbl);
+  for (int b = 0; b < nbl; ++b) offsets[b] = P.off[b];
+  offsets[nbl] = n;
+  return HJB_OK;
+}
+
 int hjb_block_owners(int32_t strategy, int32_t p, int32_t world, int32_t sweeps, int32_t *owner) {
   if (p < 1 || world < 1 || p < world || sweeps < 0 || !owner ||
       (strategy != HJB_MODULUS && strategy != HJB_ROUND_ROBIN))

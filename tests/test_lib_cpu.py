@@ -105,3 +105,17 @@ def test_orthogonality_argument_validation():
         _lib.check(_lib.HJB_EINVAL)
     assert L.hjb_orthogonality(_lib.HJB_C128, 4, 0, dummy, 4, ctypes.byref(out), None) == _lib.HJB_OK
     assert out.value == 0.0
+
+
+def test_native_partition_matches_reference_rule():
+    """hjb_partition (the partition hjb_solve uses) == blocking.py:63-68 as
+    restated by the oracle, for ragged and exact splits."""
+    import oracle as O
+    for n in (1, 7, 20, 64, 100, 2048, 4097):
+        for nbl in (1, 2, 3, 6, 16, 64):
+            if nbl > n:
+                with pytest.raises(ValueError):
+                    P.uniform_partition(n, nbl)
+                continue
+            assert list(P.uniform_partition(n, nbl).sizes) == O.uniform_sizes(n, nbl)
+    assert P.greedy_partition(10, 4).sizes == (4, 4, 2) and P.num_blocks(10, 4) == 3
