@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   T *inbox = reinterpret_cast<T *>(smem + Cfg::OFF_IN);         // [W][2][MSG]
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + Cfg::OFF_BAR);  // [W][full 2, empty 2]
   int *Jv = reinterpret_cast<int *>(smem + Cfg::OFF_J);
-  __shared__ int s_cnt[2], s_big[2], s_fail[2];
-  __shared__ unsigned long long s_maxt;
+  __shared__ int s_cnt[2], s_big[2], s_fail[2], s_chk[2];
+  __shared__ unsigned long long s_maxt, s_swt[2];
 
   int crank = 0;
   if constexpr (C > 1) crank = int(cg::this_cluster().block_rank());
@@ -253,6 +253,8 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     s_cnt[0] = s_cnt[1] = 0;
     s_big[0] = s_big[1] = 0;
     s_fail[0] = s_fail[1] = INT_MAX;
+    s_chk[0] = s_chk[1] = 0;
+    s_swt[0] = s_swt[1] = 0ull;
     s_maxt = 0ull;
   }
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   const double otol2 = otol * otol;
   const double qtol = a.quad_tol > 0.0 ? a.quad_tol : double(Nq) * kEpsJ;
   int my_cnt = 0, my_big = 0, my_fail = INT_MAX;
-  double my_maxt = 0.0;
+  double my_maxt = 0.0, my_swt = 0.0, prev_swt = 1.0;
   long long nrot_total = 0, big_total = 0;
   int sweeps = 0, status = PV_OK;
   long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // round, empty wait, send, full wait, receive, sweep end, rounds, t0
@@ -364,6 +366,7 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
           ++my_cnt;
           my_big += fabs(r.num) > qtol * r.den;  // |t| > quad_tol
           my_maxt = fmax(my_maxt, fabs(r.num) / r.den);
+          my_swt = fmax(my_swt, fabs(r.num) / r.den);
         }
       } else {
         rot = false;
@@ -572,6 +575,57 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   };
 
   // ---------------------------------------------------------- inner sweeps
+  // Final-sweep Gram check: after a sweep whose largest |t| is below
+  // 2 sqrt(orth_tol) the next sweep is almost surely the zero-rotation sweep
+  // that ends the loop (rotations.py:220-222).  Instead of running its N - 1
+  // rounds, every warp tests its columns against all later columns with the
+  // skip test of _kernels.py:57 (D = colnorms^2 at the sweep start,
+  // rotations.py:217); if every pair passes, the sweep applies no rotation --
+  // the outcome of running it -- and counts as a sweep; otherwise it runs.
+  // Pre-pass blocks (diagonal after the first outer sweep) are checked before
+  // their first sweep.
+  const double chk_thr = 2.0 * sqrt(otol);
+  double *dsc = a.dscr ? a.dscr + int64_t(item_id) * ld : nullptr;
+  auto gram_check = [&](int slot) -> bool {
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      const int col = col_of(c);
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) Rf[(lane + 32 * u) + int64_t(col) * ld] = V[u][c];
+      if (lane == 0) dsc[col] = D[c];
+    }
+    jb_cluster_sync<C>();
+    bool bad = false;
+    for (int oc = 0; oc < Nq; ++oc) {
+      T x[RPL];
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) x[u] = __ldcg(Rf + (lane + 32 * u) + int64_t(oc) * ld);
+      const double dother = __ldcg(dsc + oc);
+      sfor<CPW>([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        if (live[c] && oc > col_of(c)) {  // every pair once: the owner of the lower column checks it
+          T d0 = S<T>::zero(), d1 = S<T>::zero();
+#pragma unroll
+          for (int u = 0; u < RPL; u += 2) {
+            d0 = cfma(V[u][c], x[u], d0);
+            if (u + 1 < RPL) d1 = cfma(V[u + 1][c], x[u + 1], d1);
+          }
+          T dd = add(d0, d1);
+#pragma unroll
+          for (int dist = 16; dist >= 1; dist >>= 1) dd = add(dd, shfl_xor(dd, dist));
+          bad |= !(abs2(dd) <= otol2 * (D[c] * dother));
+        }
+      });
+    }
+    if (bad && lane == 0) atomicOr(&s_chk[slot], 1);
+    jb_cluster_sync<C>();
+    int any_bad = 0;
+#pragma unroll
+    for (int r = 0; r < C; ++r)
+      any_bad |= C > 1 ? *cg::this_cluster().map_shared_rank(&s_chk[slot], r) : s_chk[slot];
+    return any_bad == 0;
+  };
+
   for (int sw = 0; sw < a.max_sweeps; ++sw) {
     const int nsweep = sw + 1;  // the reference counts sweeps from 1
     ++sweeps;
@@ -592,6 +646,12 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
 #pragma unroll
         for (int c = 0; c < CPW; ++c) D[c] += __shfl_xor_sync(0xffffffffu, D[c], dist);
     }
+    if (dsc && ((sw > 0 && prev_swt <= chk_thr) || (sw == 0 && nj == 0))) {
+      const long long g0 = JCLK();
+      const bool ok = gram_check(sw & 1);
+      if (HJB_JAC_PROF) pf[5] += JCLK() - g0;
+      if (ok) break;  // the zero-rotation sweep, counted
+    }
     phase_a();
     for (int s = 1; s < NBL - 1; ++s) {
       exchange(nsweep);
@@ -611,23 +671,34 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
         if (wf != INT_MAX) atomicMin(&s_fail[par], wf);
       }
       my_cnt = my_big = 0;
+      double wt = my_swt;
+#pragma unroll
+      for (int dist = 16; dist >= 1; dist >>= 1) wt = fmax(wt, __shfl_xor_sync(0xffffffffu, wt, dist));
+      if (lane == 0 && wt > 0.0) atomicMax(&s_swt[par], static_cast<unsigned long long>(__double_as_longlong(wt)));
+      my_swt = 0.0;
     }
     jb_cluster_sync<C>();
     long long tot = 0;
+    unsigned long long swt = 0ull;
     int big = 0, fl = INT_MAX;
 #pragma unroll
     for (int r = 0; r < C; ++r) {
       const int *pc = C > 1 ? cg::this_cluster().map_shared_rank(&s_cnt[par], r) : &s_cnt[par];
       const int *pb = C > 1 ? cg::this_cluster().map_shared_rank(&s_big[par], r) : &s_big[par];
       const int *pf = C > 1 ? cg::this_cluster().map_shared_rank(&s_fail[par], r) : &s_fail[par];
+      const unsigned long long *pt = C > 1 ? cg::this_cluster().map_shared_rank(&s_swt[par], r) : &s_swt[par];
       tot += *pc;
       big += *pb;
       fl = min(fl, *pf);
+      swt = max(swt, *pt);
     }
+    prev_swt = __longlong_as_double(static_cast<long long>(swt));
     if (tid == 0) {  // reset the other parity for the next sweep (read only after the next cluster sync)
       s_cnt[par ^ 1] = 0;
       s_big[par ^ 1] = 0;
       s_fail[par ^ 1] = INT_MAX;
+      s_chk[par ^ 1] = 0;
+      s_swt[par ^ 1] = 0ull;
     }
     big_total += big;
     nrot_total += tot;

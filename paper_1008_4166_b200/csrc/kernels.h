@@ -43,6 +43,7 @@ struct PivotArgs {
   void *gchk;         // [count][16][blocks][16] Gram-check partials (L2 scratch), may be null
   int mode;           // PV_FULL: whole pivot; PV_PROLOGUE: R0 -> R0g only; PV_EPILOGUE: W = R0^-1 R_final
   void *R0g;          // [count][nmax*nmax] R0 (prologue output / epilogue input)
+  void *dscr;         // [count][nmax] doubles: the Jacobi kernel's Gram-check scratch
 };
 // cluster: 0 = automatic choice
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used);
@@ -71,6 +72,7 @@ struct JacobiArgs {
   int max_sweeps;
   int64_t *stats;        // [count][ST_N]: status/fallback in, counters out
   long long *prof;       // optional per-warp phase clocks [count*C*W][8] (HJB_JAC_PROF builds)
+  double *dscr;          // [count][ld] column norms of the final-sweep Gram check (null: no check)
 };
 struct JacShape {
   int c, w, spw;  // cluster size, warps per CTA, pairs per warp (nmax = 2 c w spw)

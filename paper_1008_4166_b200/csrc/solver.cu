@@ -82,7 +82,7 @@ struct HBuf {
 };
 
 struct Workspace {
-  DBuf G, items, A, D, W, U, Gc, R0, stats, signs, red, lam, flag;
+  DBuf G, items, A, D, W, U, Gc, R0, Dc, stats, signs, red, lam, flag;
   HBuf stats_h, red_h;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> events;
@@ -172,6 +172,7 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   j.max_sweeps = pa.max_sweeps;
   j.stats = pa.stats;
   j.prof = prof;
+  j.dscr = static_cast<double *>(pa.dscr);
   JacShape sh = jacobi_default_shape(cx, pa.nmax, pa.count);
   if (cluster_req > 0 && cluster_req != sh.c && !jacobi_shape_for(pa.nmax, cluster_req, &sh))
     return cudaErrorInvalidConfiguration;  // no instantiated shape with that cluster size
@@ -241,6 +242,7 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   pa.uscr = c.ws->U.p;
   pa.gchk = c.ws->Gc.p;
   pa.R0g = c.ws->R0.p;
+  pa.dscr = c.ws->Dc.p;
   int used = 0;
   CK(launch_inner(c.cx, pa, c.cluster_req, c.st, &used, &c.launches));
   c.cluster = used;
@@ -269,6 +271,7 @@ int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_co
   CK(ws.U.reserve(size_t(max_count) * (nmax / 2) * (nmax / 2 + 1) * w));  // pivot factor U (L2 scratch)
   CK(ws.Gc.reserve(size_t(max_count) * pivot_check_elems(nmax) * w));    // final-sweep Gram check
   CK(ws.R0.reserve(size_t(max_count) * nmax * nmax * w));                 // R0 between prologue and Jacobi
+  CK(ws.Dc.reserve(size_t(max_count) * nmax * sizeof(double)));          // Jacobi final-sweep check norms
   return HJB_OK;
 }
 
@@ -859,6 +862,8 @@ int hjb_pivot(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_
   pa.gchk = ws.Gc.p;
   CK(ws.R0.reserve(size_t(count) * nmax * nmax * (dtype == HJB_C128 ? 16 : 8)));
   pa.R0g = ws.R0.p;
+  CK(ws.Dc.reserve(size_t(count) * nmax * sizeof(double)));
+  pa.dscr = ws.Dc.p;
   int launches = 0;
   cudaError_t e = launch_inner(dtype == HJB_C128, pa, cluster, st, nullptr, &launches);
   if (e == cudaErrorInvalidConfiguration) return fail(HJB_EINVAL, "hjb_pivot: unsupported cluster size");
@@ -895,6 +900,8 @@ int hjb_jacobi(int32_t dtype, const int32_t *items_host, int32_t count, int32_t 
   j.max_sweeps = max_sweeps;
   j.stats = stats;
   j.prof = g_pivot_prof;
+  CK(ws.Dc.reserve(size_t(count) * nmax * sizeof(double)));
+  j.dscr = static_cast<double *>(ws.Dc.p);
   JacShape sh = jacobi_default_shape(cx, nmax, count);
   if (cluster > 0 && cluster != sh.c && !jacobi_shape_for(nmax, cluster, &sh))
     return fail(HJB_EINVAL, "hjb_jacobi: no Jacobi shape with that cluster size");
