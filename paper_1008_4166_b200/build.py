@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.environ.get("HJB_LIB") or os.path.join(HERE, "libhjb200.so")
 OBJ = os.path.join(ROOT, "build", "obj" + os.environ.get("HJB_OBJ_TAG", ""))
-SOURCES = ["schedule.cpp", "gram.cu", "pivot.cu", "jacobi.cu", "update.cu", "solver.cu"]
+SOURCES = ["schedule.cpp", "gram.cu", "pivot.cu", "factor.cu", "jacobi.cu", "update.cu", "solver.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -13,15 +13,18 @@ struct GramArgs {
   const Item *items;
   int count;
   int bmax;
-  int tiles;        // tiles per dimension (set by launch_gram)
-  int splits;       // split-K factor
-  int64_t ksplit;   // rows per split (multiple of the K chunk)
   void *A;          // [count][bmax*bmax] final Gram, column-major ld bmax
   double *D;        // [count][2*bmax] final column norms^2
+  void *Apart;      // split-K partial scratch (gram_scratch_bytes), may be null: one split
+  size_t part_bytes;
+  // set by launch_gram
+  int tiles_m, tiles_n;  // tiles per dimension
+  int splits;            // K splits (whole K chunks, sizes differ by at most one chunk)
+  double *Dpart;
 };
-cudaError_t launch_gram(bool cx, GramArgs a, cudaStream_t st);
-int gram_tile(int bmax);
-int gram_kc(bool cx);
+// splits_used (optional): the K split count the launch chose
+cudaError_t launch_gram(bool cx, GramArgs a, cudaStream_t st, int *splits_used = nullptr);
+size_t gram_scratch_bytes(bool cx, int count, int bmax);
 
 struct PivotArgs {
   const void *G;
@@ -56,6 +59,11 @@ size_t pivot_check_elems(int nmax);
 // the (cluster, threads) launch_pivot picks when not told (honours hjb_tune)
 int pivot_choose_cluster(bool cx, int nmax, int count);
 int pivot_choose_threads(bool cx, int nmax, int c);  // Gram-check scratch elements per item
+
+// factor.cu: one-CTA-per-pivot prologue (R0) and column-sliced epilogue
+// (W = R0^-1 R_final) around the Jacobi kernel
+cudaError_t launch_factor_prologue(bool cx, const PivotArgs &a, cudaStream_t st);
+cudaError_t launch_factor_epilogue(bool cx, const PivotArgs &a, cudaStream_t st);
 
 cudaError_t launch_plane_rotations(bool cx, int count, const double *arr, const double *ass, const void *ars,
                                    const int8_t *same, double *out, cudaStream_t st);

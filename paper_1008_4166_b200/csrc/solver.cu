@@ -82,7 +82,7 @@ struct HBuf {
 };
 
 struct Workspace {
-  DBuf G, items, A, D, W, U, Gc, R0, Dc, stats, signs, red, lam, flag;
+  DBuf G, items, A, D, W, U, Gc, R0, Dc, Gp, stats, signs, red, lam, flag;
   HBuf stats_h, red_h;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> events;
@@ -119,29 +119,21 @@ Partition uniform_partition(int64_t n, int nbl) {  // blocking.py:63-68
   return P;
 }
 
-// K splits of one Gram tile = the cluster size of gram_kernel (1 .. 16):
-// about two CTAs per SM, at least one K chunk per split
-int gram_splits(int count, int tiles, int64_t m, int kc, int64_t *ksplit) {
-  const int64_t chunks = (m + kc - 1) / kc;
-  const int64_t per = int64_t(count) * tiles * tiles;
-  static const int smax = [] {  // tuning override (experiments only)
-    const char *e = std::getenv("HJB_GRAM_SPLITS_MAX");
-    const int v = e ? std::atoi(e) : 16;
-    return (v >= 1 && v <= 16) ? v : 16;
-  }();
-  int s = 1;
-  while (2 * s <= smax && per * (2 * s) <= 2 * 148 + per / 2 && 2 * s <= chunks) s *= 2;
-  const int64_t cps = (chunks + s - 1) / s;  // chunks per split
-  *ksplit = cps * kc;
-  return s;
-}
-
 // Inner level: the ring-of-rings Jacobi kernel between the pivot kernel's
 // prologue and epilogue (default), or the round-1 single pivot kernel
 // (HJB_PIVOT_V1=1, kept for A/B measurements).
 bool inner_v1() {
   static const bool v1 = [] {
     const char *e = std::getenv("HJB_PIVOT_V1");
+    return e && std::atoi(e) != 0;
+  }();
+  return v1;
+}
+
+// round-1 prologue / epilogue inside the cluster pivot kernel (HJB_FACTOR_V1=1, A/B only)
+bool factor_v1() {
+  static const bool v1 = [] {
+    const char *e = std::getenv("HJB_FACTOR_V1");
     return e && std::atoi(e) != 0;
   }();
   return v1;
@@ -157,7 +149,7 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   long long *prof = pa.prof;  // phase clocks are the Jacobi kernel's
   pa.prof = nullptr;
   pa.mode = PV_PROLOGUE;
-  cudaError_t e = launch_pivot(cx, pa, 0, st, nullptr);
+  cudaError_t e = factor_v1() ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_prologue(cx, pa, st);
   if (e != cudaSuccess) return e;
   JacobiArgs j{};
   j.items = pa.items;
@@ -181,7 +173,7 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   if (e != cudaSuccess) return e;
   pa.mode = PV_EPILOGUE;
   *launches += 3;
-  return launch_pivot(cx, pa, 0, st, nullptr);
+  return factor_v1() ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_epilogue(cx, pa, st);
 }
 
 struct PhaseCtx {
@@ -202,11 +194,6 @@ struct PhaseCtx {
 int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, void *Rout,
               cudaEvent_t *ev) {
   if (count == 0) return HJB_OK;
-  const int tile = gram_tile(c.bmax);
-  const int tiles = (c.bmax + tile - 1) / tile;
-  int64_t ksplit = 0;
-  const int splits = gram_splits(count, tiles, c.m, gram_kc(c.cx), &ksplit);
-  c.splits_used = splits;
   GramArgs g{};
   g.G = c.G;
   g.ldg = c.ld;
@@ -214,13 +201,15 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   g.items = items_d;
   g.count = count;
   g.bmax = c.bmax;
-  g.splits = splits;
-  g.ksplit = ksplit;
   g.A = c.ws->A.p;
   g.D = static_cast<double *>(c.ws->D.p);
+  g.Apart = c.ws->Gp.p;
+  g.part_bytes = c.ws->Gp.n;
   if (ev) CK(cudaEventRecord(ev[0], c.st));
-  CK(launch_gram(c.cx, g, c.st));
-  ++c.launches;
+  int splits = 1;
+  CK(launch_gram(c.cx, g, c.st, &splits));
+  c.splits_used = splits;
+  c.launches += splits > 1 ? 2 : 1;
   if (ev) CK(cudaEventRecord(ev[1], c.st));
   PivotArgs pa{};
   pa.G = c.G;
@@ -272,6 +261,7 @@ int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_co
   CK(ws.Gc.reserve(size_t(max_count) * pivot_check_elems(nmax) * w));    // final-sweep Gram check
   CK(ws.R0.reserve(size_t(max_count) * nmax * nmax * w));                 // R0 between prologue and Jacobi
   CK(ws.Dc.reserve(size_t(max_count) * nmax * sizeof(double)));          // Jacobi final-sweep check norms
+  CK(ws.Gp.reserve(std::min<size_t>(gram_scratch_bytes(cx, max_count, bmax), size_t(768) << 20)));  // Gram split-K partials
   return HJB_OK;
 }
 
@@ -807,8 +797,6 @@ int hjb_gram(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_t
   if (int rc = upload_items(ws, items_host, count, st)) return rc;
   const bool cx = dtype == HJB_C128;
   if (int rc = reserve_phase_buffers(ws, cx, bmax, std::max(64, pivot_nmax(bmax)), count, m)) return rc;
-  const int tile = gram_tile(bmax);
-  const int tiles = (bmax + tile - 1) / tile;
   GramArgs g{};
   g.G = G;
   g.ldg = ldg;
@@ -816,9 +804,10 @@ int hjb_gram(int32_t dtype, int64_t m, const void *G, int64_t ldg, const int32_t
   g.items = static_cast<const Item *>(ws.items.p);
   g.count = count;
   g.bmax = bmax;
-  g.splits = gram_splits(count, tiles, m, gram_kc(cx), &g.ksplit);
   g.A = A;
   g.D = D;
+  g.Apart = ws.Gp.p;
+  g.part_bytes = ws.Gp.n;
   CK(launch_gram(cx, g, st));
   CK(cudaStreamSynchronize(st));
   return HJB_OK;
@@ -981,8 +970,6 @@ int hjb_orthogonality(int32_t dtype, int64_t m, int64_t n, const void *U, int64_
   CK(ws.red.reserve(sizeof(unsigned long long)));
   unsigned long long *acc = static_cast<unsigned long long *>(ws.red.p);
   CK(cudaMemsetAsync(acc, 0, sizeof(unsigned long long), st));
-  const int tile = gram_tile(bw);
-  const int tiles = (bw + tile - 1) / tile;
   for (size_t s0 = 0; s0 < all.size(); s0 += chunk) {
     const int count = int(std::min<size_t>(chunk, all.size() - s0));
     const Item *items_d = static_cast<const Item *>(ws.items.p) + s0;
@@ -993,9 +980,10 @@ int hjb_orthogonality(int32_t dtype, int64_t m, int64_t n, const void *U, int64_
     g.items = items_d;
     g.count = count;
     g.bmax = bw;
-    g.splits = gram_splits(count, tiles, m, gram_kc(cx), &g.ksplit);
     g.A = ws.A.p;
     g.D = static_cast<double *>(ws.D.p);
+    g.Apart = ws.Gp.p;
+    g.part_bytes = ws.Gp.n;
     CK(launch_gram(cx, g, st));
     CK(launch_orth_max(cx, items_d, count, bw, ws.A.p, acc, st));
   }
