@@ -64,6 +64,9 @@ typedef struct {
 } hjb_problem;
 
 #define HJB_FLAG_PHASE_TIMES 1   /* record per-phase device times (adds events) */
+#define HJB_FLAG_VARIANT_B 8     /* block-oriented variants 2B / 3B (parallel.py:160-174, 199-200):
+                                    no F pre-pass, dense pair factor, one annihilation
+                                    cycle per step; default: the F variants (2F / 3F) */
 #define HJB_FLAG_GATHER_ROOT 4   /* multi-GPU: only rank 0 receives the whole G_out
                                     (other ranks keep the blocks they hold);
                                     default: every rank receives it */

@@ -22,6 +22,7 @@ HJB_MODULUS, HJB_ROUND_ROBIN = 0, 1
 HJB_HOST, HJB_DEVICE = 0, 1
 HJB_FLAG_PHASE_TIMES = 1
 HJB_FLAG_GATHER_ROOT = 4
+HJB_FLAG_VARIANT_B = 8
 ST_N = 8
 
 

@@ -126,5 +126,12 @@ enum { PV_OK = 0, PV_INDEFINITE = 1, PV_CHOL = 2 };
 // its prologue (structured Cholesky -> R0) and epilogue (W = R0^-1 R_final)
 // around the Jacobi kernel
 enum { PV_FULL = 0, PV_PROLOGUE = 1, PV_EPILOGUE = 2 };
+// factor.cu prologue input: the structured pair factor of the F variants
+// (A_ij and the block norms, blocking.py:115-138) or the dense pair Gram of
+// the B variants (three Gram items per pair: A_ii, A_jj, A_ij; parallel.py:199-200)
+enum { FP_STRUCTURED = 0, FP_DENSE_PAIR = 1 };
+// Jacobi kernel modes: sweeps until no rotation (jacobi_diagonalize), one
+// cycle over all pairs, one cycle over the cross pairs of the two blocks
+enum { JAC_CONVERGE = 0, JAC_ONE_CYCLE = 1, JAC_CROSS = 2 };
 
 }  // namespace hjb

@@ -337,6 +337,190 @@ __global__ void __launch_bounds__(ProCfg<T, B>::NT, 1) factor_prologue_kernel(Pi
   (void)nu;
 }
 
+// ------------------------------------------------------------------ dense pair (B variants)
+// R0 = chol(gram([G_i G_j])) (parallel.py:199-200) by blocks:
+//   R_ii = chol(herm(A_ii)),  X = R_ii^-H A_ij,  R_jj = chol(herm(A_jj) - X^H X).
+// A_ii, A_jj, A_ij are items 3t, 3t+1, 3t+2 of the Gram launch.  The forward
+// substitution runs on 32-column slices of A_ij in shared memory (32-row
+// blocks: DMMA for the part above the diagonal block, warp-shuffle
+// substitution inside it); X goes to the top-right block of R0 in global
+// memory and is staged back in K chunks for the Schur complement.
+template <typename T, int B>
+__global__ void __launch_bounds__(ProCfg<T, B>::NT, 1) factor_dense_pair_kernel(PivotArgs a) {
+  using Cfg = ProCfg<T, B>;
+  constexpr int NT = Cfg::NT, NW = Cfg::NW, KC = Cfg::KC, KCP = Cfg::KCP;
+  constexpr int SW = 32;                // slice width (columns of A_ij)
+  constexpr int CPW = SW / NW;          // columns per warp in the substitution
+  constexpr int LDS_ = B + 4;           // slice leading dimension
+  static_assert(SW * LDS_ <= B * KCP, "the slice buffer aliases the chunk staging buffer");
+  extern __shared__ __align__(16) unsigned char smem[];
+  T *Sp = reinterpret_cast<T *>(smem + Cfg::OFF_S);
+  T *Xs = reinterpret_cast<T *>(smem + Cfg::OFF_X);
+  T *rowk = reinterpret_cast<T *>(smem + Cfg::OFF_ROW);
+  double *piv = reinterpret_cast<double *>(smem + Cfg::OFF_LAM) + 3 * B;
+
+  const int item_id = blockIdx.x;
+  const Item it = a.items[item_id];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ni = it.ni, nj = it.nj, N = ni + nj;
+  const int bmax = a.bmax, ld = a.nmax;
+  const int64_t asz = int64_t(bmax) * bmax;
+  const T *Aii = reinterpret_cast<const T *>(a.A) + (int64_t(item_id) * 3 + 0) * asz;
+  const T *Ajj = reinterpret_cast<const T *>(a.A) + (int64_t(item_id) * 3 + 1) * asz;
+  const T *Aij = reinterpret_cast<const T *>(a.A) + (int64_t(item_id) * 3 + 2) * asz;
+  T *R0 = reinterpret_cast<T *>(a.R0g) + int64_t(item_id) * ld * ld;
+  int status = PV_OK;
+
+  auto load_herm = [&](const T *A, int n) {
+    for (int e = tid; e < n * n; e += NT) {
+      const int i = e % n, l = e / n;
+      if (i > l) continue;
+      Sp[pk(i, l)] = i == l ? scale(S<T>::one(), re(A[i + int64_t(i) * bmax]))
+                            : scale(add(A[i + int64_t(l) * bmax], conjv(A[l + int64_t(i) * bmax])), 0.5);
+    }
+  };
+  for (int e = tid; e < ld * ld; e += NT) R0[e] = S<T>::zero();
+  load_herm(Aii, ni);
+  __syncthreads();
+  if (!chol_tile<T, B, NT>(Sp, ni, rowk, piv)) status = PV_CHOL;
+  if (status == PV_OK) {
+    for (int e = tid; e < ni * ni; e += NT) {
+      const int g = e % ni, c = e / ni;
+      if (g <= c) R0[g + int64_t(c) * ld] = Sp[pk(g, c)];
+    }
+    // ---- X = R_ii^-H A_ij, slice by slice ----
+    T *Xl = Xs;  // [SW][LDS_]
+    const int nblk = (ni + 31) / 32;
+    for (int c0 = 0; c0 < nj; c0 += SW) {
+      __syncthreads();
+      for (int e = tid; e < SW * B; e += NT) {
+        const int r = e % B, c = e / B;
+        Xl[c * LDS_ + r] = (r < ni && c0 + c < nj) ? Aij[r + int64_t(c0 + c) * bmax] : S<T>::zero();
+      }
+      __syncthreads();
+      for (int I = 0; I < nblk; ++I) {
+        const int r0 = 32 * I;
+        if (I > 0) {
+          // T_I -= (R_ii^H)[I rows, h] X[h, :], h < r0: 32 x SW output, 16 fragments over the warps
+          for (int f = warp; f < 16; f += NW) {
+            const int mi = f >> 2, nn = f & 3;
+            HAcc<T> acc;
+            acc.zero();
+            const int row = r0 + mi * 8 + (lane >> 2);
+            const T *bp = Xl + (nn * 8 + (lane >> 2)) * LDS_ + (lane & 3);
+            for (int h = 0; h < r0; h += 4) {
+              const int hh = h + (lane & 3);
+              const T fa = row < ni ? Sp[pk(hh, row)] : S<T>::zero();  // R_ii[h][row], h < row
+              acc.mma(fa, bp[h]);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              T *pp = Xl + (nn * 8 + 2 * (lane & 3) + q) * LDS_ + r0 + mi * 8 + (lane >> 2);
+              *pp = sub(*pp, acc.get(q));
+            }
+          }
+          __syncthreads();
+        }
+        // forward substitution inside the diagonal block: lane s holds row r0 + s
+        {
+          const int row = r0 + lane;
+          T rr[32];
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            rr[r] = (r < lane && row < ni) ? conjv(Sp[pk(r0 + r, row)]) : S<T>::zero();
+          const double rinv = row < ni ? 1.0 / re(Sp[pk(row, row)]) : 0.0;
+          T t[CPW];
+#pragma unroll
+          for (int j = 0; j < CPW; ++j) t[j] = Xl[(warp * CPW + j) * LDS_ + row];
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+#pragma unroll
+            for (int j = 0; j < CPW; ++j) {
+              const T xr = shfl_idx(scale(t[j], rinv), r);
+              if (lane == r) t[j] = xr;
+              if (lane > r) t[j] = sub(t[j], mul(rr[r], xr));
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < CPW; ++j) Xl[(warp * CPW + j) * LDS_ + row] = t[j];
+        }
+        __syncthreads();
+      }
+      for (int e = tid; e < SW * ni; e += NT) {
+        const int r = e % ni, c = e / ni;
+        if (c0 + c < nj) R0[r + int64_t(ni + c0 + c) * ld] = Xl[c * LDS_ + r];
+      }
+    }
+    __syncthreads();
+    // ---- S = herm(A_jj) - X^H X, R_jj = chol(S) ----
+    load_herm(Ajj, nj);
+    constexpr int TJ = B / 32, NTILE = (B / 16) * TJ;
+    for (int h0 = 0; h0 < ni; h0 += KC) {
+      __syncthreads();
+      for (int e = tid; e < B * KC; e += NT) {
+        const int k = e % KC, l = e / KC;
+        const int h = h0 + k;
+        Xs[l * KCP + k] = (h < ni && l < nj) ? R0[h + int64_t(ni + l) * ld] : S<T>::zero();
+      }
+      __syncthreads();
+      for (int t = warp; t < NTILE; t += NW) {
+        const int ti = t / TJ, tj = t % TJ;
+        if (16 * ti >= 32 * (tj + 1) || 16 * ti >= nj || 32 * tj >= nj) continue;
+        HAcc<T> acc[2][4];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nn = 0; nn < 4; ++nn) acc[mi][nn].zero();
+#pragma unroll 2
+        for (int kk = 0; kk < KC; kk += 4) {
+          T fa[2], fb[4];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) fa[mi] = Xs[((ti * 2 + mi) * 8 + (lane >> 2)) * KCP + kk + (lane & 3)];
+#pragma unroll
+          for (int nn = 0; nn < 4; ++nn) fb[nn] = Xs[((tj * 4 + nn) * 8 + (lane >> 2)) * KCP + kk + (lane & 3)];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nn = 0; nn < 4; ++nn) acc[mi][nn].mma(fa[mi], fb[nn]);
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int i = (ti * 2 + mi) * 8 + (lane >> 2);
+              const int l = (tj * 4 + nn) * 8 + 2 * (lane & 3) + q;
+              if (i <= l && l < nj) Sp[pk(i, l)] = sub(Sp[pk(i, l)], acc[mi][nn].get(q));
+            }
+      }
+    }
+    __syncthreads();
+    for (int c = tid; c < nj; c += NT) Sp[pk(c, c)] = scale(S<T>::one(), re(Sp[pk(c, c)]));
+    __syncthreads();
+    if (!chol_tile<T, B, NT>(Sp, nj, rowk, piv)) {
+      status = PV_CHOL;
+    } else {
+      for (int e = tid; e < nj * nj; e += NT) {
+        const int g = e % nj, c = e / nj;
+        if (g <= c) R0[(ni + g) + int64_t(ni + c) * ld] = Sp[pk(g, c)];
+      }
+    }
+  }
+  if (tid == 0) {
+    int64_t *st = a.stats + int64_t(item_id) * ST_N;
+    st[ST_NROT] = 0;
+    st[ST_NBIG] = 0;
+    st[ST_MAXT] = 0;
+    st[ST_SWEEPS] = 0;
+    st[ST_STATUS] = status;
+    st[ST_FR] = -1;
+    st[ST_FS] = -1;
+    st[ST_FALLBACK] = 1;  // R0 is a general upper-triangular factor for the epilogue
+  }
+  (void)N;
+}
+
 // ------------------------------------------------------------------ epilogue
 
 template <typename T>
@@ -444,9 +628,9 @@ __global__ void __launch_bounds__(256) factor_epilogue_kernel(PivotArgs a) {
 template <typename T, int B>
 cudaError_t launch_prologue_t(const PivotArgs &a, cudaStream_t st) {
   using Cfg = ProCfg<T, B>;
-  auto k = factor_prologue_kernel<T, B>;
-  static DeviceFlags attr_flags;
-  bool *attr = attr_flags.here();
+  auto k = a.fp_input == FP_DENSE_PAIR ? factor_dense_pair_kernel<T, B> : factor_prologue_kernel<T, B>;
+  static DeviceFlags attr_flags[2];
+  bool *attr = attr_flags[a.fp_input == FP_DENSE_PAIR].here();
   if (!attr) return cudaErrorInvalidDevice;
   if (!*attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));

@@ -284,12 +284,17 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   pf[7] = JCLK();
 
   // per-slot column state: J sign and "real column" flag (ids >= Nq are padding)
+  // JAC_CROSS (the B variants' annihilation pass, parallel.py:170-174 /
+  // _kernels.py:41-52 with diag_bl = False): only pairs with one column in
+  // each block rotate; the sweep still visits every pair of columns
+  const bool cross = a.mode == JAC_CROSS;
   int sg[CPW];
-  bool live[CPW];
+  bool live[CPW], side[CPW];
   auto refresh_slot = [&](int c) {
     const int col = col_of(c);
     sg[c] = Jv[col];
     live[c] = col < Nq;
+    side[c] = col >= ni;
   };
   sfor<CPW>([&](auto c) { refresh_slot(c); });
 
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
         ds = D[B];
         sr = sg[A];
         ss = sg[B];
-        lv = live[A] && live[B];
+        lv = live[A] && live[B] && (!cross || side[A] != side[B]);
         ar = A;
         as = B;
       }
@@ -585,7 +590,7 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
   // Pre-pass blocks (diagonal after the first outer sweep) are checked before
   // their first sweep.
   const double chk_thr = 2.0 * sqrt(otol);
-  double *dsc = a.dscr ? a.dscr + int64_t(item_id) * ld : nullptr;
+  double *dsc = (a.dscr && a.mode == JAC_CONVERGE) ? a.dscr + int64_t(item_id) * ld : nullptr;
   auto gram_check = [&](int slot) -> bool {
 #pragma unroll
     for (int c = 0; c < CPW; ++c) {
@@ -708,7 +713,8 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
       my_fail = fl;
       break;
     }
-    if (tot == 0 || sw + 1 == a.max_sweeps) break;
+    // one cycle only for the B variants (tol.with_max_sweeps(1), parallel.py:162-174)
+    if (tot == 0 || sw + 1 == a.max_sweeps || a.mode != JAC_CONVERGE) break;
     exchange(nsweep);  // the sweep's last exchange (parallel.py:234-237)
   }
   // max |t| over the cluster

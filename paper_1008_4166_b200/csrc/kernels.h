@@ -47,6 +47,8 @@ struct PivotArgs {
   int mode;           // PV_FULL: whole pivot; PV_PROLOGUE: R0 -> R0g only; PV_EPILOGUE: W = R0^-1 R_final
   void *R0g;          // [count][nmax*nmax] R0 (prologue output / epilogue input)
   void *dscr;         // [count][nmax] doubles: the Jacobi kernel's Gram-check scratch
+  int fp_input;       // factor prologue: FP_STRUCTURED (A[item], D[item]) or FP_DENSE_PAIR
+                      // (A[3 item + 0/1/2] = A_ii, A_jj, A_ij of the pair)
 };
 // cluster: 0 = automatic choice
 cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t st, int *cluster_used);
@@ -81,6 +83,7 @@ struct JacobiArgs {
   int64_t *stats;        // [count][ST_N]: status/fallback in, counters out
   long long *prof;       // optional per-warp phase clocks [count*C*W][8] (HJB_JAC_PROF builds)
   double *dscr;          // [count][ld] column norms of the final-sweep Gram check (null: no check)
+  int mode;              // JAC_CONVERGE (F variants), JAC_ONE_CYCLE / JAC_CROSS (B variants)
 };
 struct JacShape {
   int c, w, spw;  // cluster size, warps per CTA, pairs per warp (nmax = 2 c w spw)

@@ -82,7 +82,7 @@ struct HBuf {
 };
 
 struct Workspace {
-  DBuf G, items, A, D, W, U, Gc, R0, Dc, Gp, stats, signs, red, lam, flag;
+  DBuf G, items, gitems, A, D, W, U, Gc, R0, Dc, Gp, stats, signs, red, lam, flag;
   HBuf stats_h, red_h;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> events;
@@ -140,8 +140,10 @@ bool factor_v1() {
 }
 
 // the three pivot-phase launches of one batch (or the single v1 launch)
-cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st, int *cluster_used, int *launches) {
-  if (inner_v1()) {
+cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st, int *cluster_used, int *launches,
+                         int jac_mode = JAC_CONVERGE) {
+  const bool vb = pa.fp_input == FP_DENSE_PAIR;  // B variants: always the round-2 kernels
+  if (inner_v1() && !vb) {
     pa.mode = PV_FULL;
     ++*launches;
     return launch_pivot(cx, pa, cluster_req, st, cluster_used);
@@ -149,7 +151,7 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   long long *prof = pa.prof;  // phase clocks are the Jacobi kernel's
   pa.prof = nullptr;
   pa.mode = PV_PROLOGUE;
-  cudaError_t e = factor_v1() ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_prologue(cx, pa, st);
+  cudaError_t e = (factor_v1() && !vb) ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_prologue(cx, pa, st);
   if (e != cudaSuccess) return e;
   JacobiArgs j{};
   j.items = pa.items;
@@ -165,6 +167,7 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   j.stats = pa.stats;
   j.prof = prof;
   j.dscr = static_cast<double *>(pa.dscr);
+  j.mode = jac_mode;
   JacShape sh = jacobi_default_shape(cx, pa.nmax, pa.count);
   if (cluster_req > 0 && cluster_req != sh.c && !jacobi_shape_for(pa.nmax, cluster_req, &sh))
     return cudaErrorInvalidConfiguration;  // no instantiated shape with that cluster size
@@ -173,7 +176,7 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   if (e != cudaSuccess) return e;
   pa.mode = PV_EPILOGUE;
   *launches += 3;
-  return factor_v1() ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_epilogue(cx, pa, st);
+  return (factor_v1() && !vb) ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_epilogue(cx, pa, st);
 }
 
 struct PhaseCtx {
@@ -191,15 +194,18 @@ struct PhaseCtx {
 };
 
 // Gram -> pivot -> update for one batch of items (device item table).
+// gram_items_d != null: B variants -- three Gram items per pair (A_ii, A_jj,
+// A_ij) feed the dense pair factor, and the Jacobi kernel runs one cycle
+// (jac_mode) instead of sweeping to convergence (parallel.py:160-174, 199-200)
 int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, void *Rout,
-              cudaEvent_t *ev) {
+              cudaEvent_t *ev, const Item *gram_items_d = nullptr, int jac_mode = JAC_CONVERGE) {
   if (count == 0) return HJB_OK;
   GramArgs g{};
   g.G = c.G;
   g.ldg = c.ld;
   g.m = c.m;
-  g.items = items_d;
-  g.count = count;
+  g.items = gram_items_d ? gram_items_d : items_d;
+  g.count = gram_items_d ? 3 * count : count;
   g.bmax = c.bmax;
   g.A = c.ws->A.p;
   g.D = static_cast<double *>(c.ws->D.p);
@@ -232,8 +238,9 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   pa.gchk = c.ws->Gc.p;
   pa.R0g = c.ws->R0.p;
   pa.dscr = c.ws->Dc.p;
+  pa.fp_input = gram_items_d ? FP_DENSE_PAIR : FP_STRUCTURED;
   int used = 0;
-  CK(launch_inner(c.cx, pa, c.cluster_req, c.st, &used, &c.launches));
+  CK(launch_inner(c.cx, pa, c.cluster_req, c.st, &used, &c.launches, jac_mode));
   c.cluster = used;
   if (ev) CK(cudaEventRecord(ev[2], c.st));
   UpdateArgs u{};
@@ -251,17 +258,19 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   return HJB_OK;
 }
 
-int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_count, int64_t m) {
+int reserve_phase_buffers(Workspace &ws, bool cx, int bmax, int nmax, int max_count, int64_t m,
+                          int gram_items = 0) {
   const size_t w = cx ? 16 : 8;
   (void)m;
-  CK(ws.A.reserve(size_t(max_count) * bmax * bmax * w));
-  CK(ws.D.reserve(size_t(max_count) * 2 * bmax * 8));
+  const int gcount = std::max(max_count, gram_items);  // B variants: three Gram items per pair
+  CK(ws.A.reserve(size_t(gcount) * bmax * bmax * w));
+  CK(ws.D.reserve(size_t(gcount) * 2 * bmax * 8));
   CK(ws.W.reserve(size_t(max_count) * nmax * nmax * w));
   CK(ws.U.reserve(size_t(max_count) * (nmax / 2) * (nmax / 2 + 1) * w));  // pivot factor U (L2 scratch)
   CK(ws.Gc.reserve(size_t(max_count) * pivot_check_elems(nmax) * w));    // final-sweep Gram check
   CK(ws.R0.reserve(size_t(max_count) * nmax * nmax * w));                 // R0 between prologue and Jacobi
   CK(ws.Dc.reserve(size_t(max_count) * nmax * sizeof(double)));          // Jacobi final-sweep check norms
-  CK(ws.Gp.reserve(std::min<size_t>(gram_scratch_bytes(cx, max_count, bmax), size_t(768) << 20)));  // Gram split-K partials
+  CK(ws.Gp.reserve(std::min<size_t>(gram_scratch_bytes(cx, gcount, bmax), size_t(768) << 20)));  // Gram split-K partials
   return HJB_OK;
 }
 
@@ -515,9 +524,13 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
     return fail(HJB_EINVAL, e.what());
   }
   const int q_lo = workers_lo(P, world, grank), q_hi = workers_lo(P, world, grank + 1), nloc = q_hi - q_lo;
+  // B variants (2B / 3B, parallel.py:160-174): no F pre-pass, the dense pair
+  // factor, one Jacobi cycle per step
+  const bool vb = pr->flags & HJB_FLAG_VARIANT_B;
   // layouts for sweeps s0..s1: [sweep - s0][1 + steps][nloc or 2*nloc]
   const int per_sweep_items = 2 * nloc + steps * nloc;
   std::vector<Item> items(size_t(nsw) * per_sweep_items);
+  std::vector<Item> gitems(vb ? size_t(nsw) * steps * 3 * nloc : 0);  // Gram items of the B variants
   std::vector<std::vector<Xfer>> xfers(size_t(nsw) * steps);
   try {
     for (int sw = s0; sw <= s1; ++sw) {
@@ -532,6 +545,12 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
         for (int q = q_lo; q < q_hi; ++q) {
           const int bi = ring.i_blk(q) - 1, bj = ring.j_blk(q) - 1;
           row[q - q_lo] = Item{part.off[bi], part.width[bi], part.off[bj], part.width[bj]};
+          if (vb) {
+            Item *g3 = gitems.data() + ((size_t(sw - s0) * steps + s) * nloc + (q - q_lo)) * 3;
+            g3[0] = Item{part.off[bi], part.width[bi], 0, 0};
+            g3[1] = Item{part.off[bj], part.width[bj], 0, 0};
+            g3[2] = row[q - q_lo];
+          }
         }
         std::vector<StepPlan> pl = ring.advance(sw);
         step_transfers(pl, P, world, grank, xfers[size_t(sw - s0) * steps + s]);
@@ -542,8 +561,12 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   }
   CK(ws.items.reserve(items.size() * sizeof(Item)));
   CK(cudaMemcpyAsync(ws.items.p, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice, st));
+  if (vb) {
+    CK(ws.gitems.reserve(std::max<size_t>(gitems.size(), 1) * sizeof(Item)));
+    CK(cudaMemcpyAsync(ws.gitems.p, gitems.data(), gitems.size() * sizeof(Item), cudaMemcpyHostToDevice, st));
+  }
   const int max_count = std::max(2 * nloc, 1);
-  if (int rc = reserve_phase_buffers(ws, cx, bmax, nmax, max_count, m)) return rc;
+  if (int rc = reserve_phase_buffers(ws, cx, bmax, nmax, max_count, m, vb ? 3 * nloc : 0)) return rc;
   const size_t stats_per_sweep = size_t(per_sweep_items) * ST_N;
   CK(ws.stats.reserve(2 * stats_per_sweep * sizeof(int64_t)));
   CK(ws.stats_h.reserve(stats_per_sweep * sizeof(int64_t)));
@@ -582,11 +605,16 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
     const Item *it_d = static_cast<const Item *>(ws.items.p) + size_t(sw - s0) * per_sweep_items;
     int64_t *stats_d = static_cast<int64_t *>(ws.stats.p) + size_t((sw - 1) & 1) * stats_per_sweep;
     cudaEvent_t *ev = phase_times ? &ws.events[2] : nullptr;
-    if (int rc = run_phase(ctx, it_d, 2 * nloc, stats_d, nullptr, ev)) return rc;
+    if (!vb)
+      if (int rc = run_phase(ctx, it_d, 2 * nloc, stats_d, nullptr, ev)) return rc;
     for (int s = 0; s < steps; ++s) {
       cudaEvent_t *evs = phase_times ? &ws.events[2 + 4 * (1 + s)] : nullptr;
+      const Item *git = vb ? static_cast<const Item *>(ws.gitems.p) + (size_t(sw - s0) * steps + s) * nloc * 3 : nullptr;
+      // first step of a sweep: one cycle over all pairs of the pivot; later
+      // steps: the cross pairs only (parallel.py:162-174)
       if (int rc = run_phase(ctx, it_d + 2 * nloc + s * nloc, nloc,
-                             stats_d + size_t(2 * nloc + s * nloc) * ST_N, nullptr, evs))
+                             stats_d + size_t(2 * nloc + s * nloc) * ST_N, nullptr, evs, git,
+                             !vb ? JAC_CONVERGE : (s == 0 ? JAC_ONE_CYCLE : JAC_CROSS)))
         return rc;
       const auto &xf = xfers[size_t(sw - s0) * steps + s];
       if (!xf.empty()) {
@@ -612,7 +640,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
     std::memcpy(hstats.data(), ws.stats_h.p, stats_per_sweep * sizeof(int64_t));
     int64_t rot = 0;
     int err = HJB_OK;
-    for (int t = 0; t < per_sweep_items; ++t) {
+    for (int t = vb ? 2 * nloc : 0; t < per_sweep_items; ++t) {
       const int64_t *sv = hstats.data() + size_t(t) * ST_N;
       const bool pre = t < 2 * nloc;
       const Item &itm = items[size_t(sw - s0) * per_sweep_items + t];
@@ -625,7 +653,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
       double mt;
       std::memcpy(&mt, &sv[ST_MAXT], 8);
       res->max_abs_t = std::max(res->max_abs_t, mt);
-      res->fallbacks += sv[ST_FALLBACK];
+      if (!vb) res->fallbacks += sv[ST_FALLBACK];
       if (pre) {
         res->prepass_visited += 1;
         res->prepass_updated += sv[ST_NROT] > 0;
@@ -647,7 +675,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
     }
     if (phase_times) {
       float ms = 0;
-      for (int s = 0; s < 1 + steps; ++s) {
+      for (int s = vb ? 1 : 0; s < 1 + steps; ++s) {
         cudaEvent_t *e = &ws.events[2 + 4 * s];
         if (s > 0 && nloc == 0) continue;
         CK(cudaEventElapsedTime(&ms, e[0], e[1])); tg += ms;

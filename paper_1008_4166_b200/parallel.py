@@ -1,5 +1,17 @@
-"""The 2F ring solver on B200: drop-in for the reference's
+"""The ring solver on B200: drop-in for the reference's
 ``parallel_jacobi(G, signs, SolverConfig)`` (pkg/src/hjacobi/parallel.py:255-309).
+
+Variants (parallel.py:43, 150-174).  ``2F`` / ``3F``: F pre-pass, structured
+pair factor, every pivot diagonalised until a sweep applies no rotation.
+``2B`` / ``3B``: no pre-pass, dense pair factor, one annihilation cycle per
+step (all pairs of the pivot at the first step of a sweep, the cross pairs of
+the two blocks afterwards).  The reference's three-level variants (3F / 3B)
+block the pivot's inner level into ``inner_n_t``-column sub-blocks; on the
+GPU the inner level is ALWAYS blocked -- the Jacobi kernel runs the
+reference's ring ordering over register-resident column sub-blocks, one warp
+per sub-block pair (csrc/jacobi.cu) -- so 3F runs the same kernels as 2F and
+3B the same as 2B; ``inner_n_t`` is validated but the sub-block width is the
+kernel's.
 
 The ring of p workers is not a set of threads here: every worker's block pair
 of a step is one item of a batched GPU launch (Gram -> pivot -> update), and
@@ -21,7 +33,17 @@ from .rotations import DEFAULT_TOL, DiagInfo, Tolerances
 from .strategies import MODULUS, normalize_strategy, strategy_code
 
 VARIANTS = ("2F", "2B", "3F", "3B")
-SUPPORTED_VARIANTS = ("2F",)
+SUPPORTED_VARIANTS = VARIANTS
+MAX_BLOCK_WIDTH = 128  # widest block column of the GPU kernels (pivot order 256)
+
+
+def effective_p(n: int, p: int) -> int:
+    """Ring workers actually used: ``p`` unless its blocks (n / 2p columns,
+    parallel.py:266) would be wider than the kernels' 128 columns; then the
+    smallest p whose blocks fit.  The reference has no such limit; a finer
+    partition is the same algorithm with more, narrower blocks."""
+    need = -(-n // (2 * MAX_BLOCK_WIDTH))
+    return max(p, need)
 
 
 @dataclass(frozen=True)
@@ -60,8 +82,10 @@ class SolverConfig:
             raise ValueError("first_sweep must be >= 1 and sweep_count >= 0")
 
 
-def _info_from(res: _lib.Result) -> DiagInfo:
+def _info_from(res: _lib.Result, p_eff=None) -> DiagInfo:
     stats = {k: getattr(res, k) for k, _ in _lib.Result._fields_}
+    if p_eff is not None:
+        stats["p_effective"] = p_eff
     return DiagInfo(sweeps=res.sweeps, rotations=res.rotations, big_rotations=res.big_rotations,
                     max_abs_t=res.max_abs_t, converged=bool(res.converged), stats=stats)
 
@@ -73,7 +97,7 @@ def _problem(cfg: SolverConfig, m, n, ld, cx, mem, gin, gout, signs, device, str
     pr.m, pr.n, pr.ldg = m, n, ld
     pr.G_in, pr.G_out = gin, gout
     pr.signs = signs.ctypes.data
-    pr.p = cfg.p
+    pr.p = effective_p(n, cfg.p)
     pr.strategy = strategy_code(cfg.strategy)
     pr.orth_tol = cfg.tol.orth_tol if cfg.tol.orth_tol is not None else -1.0
     pr.quad_tol = cfg.tol.quad_tol if cfg.tol.quad_tol is not None else -1.0
@@ -82,7 +106,8 @@ def _problem(cfg: SolverConfig, m, n, ld, cx, mem, gin, gout, signs, device, str
     pr.stream = stream
     pr.comm = cfg.comm.handle if cfg.comm is not None else None
     pr.flags = (_lib.HJB_FLAG_PHASE_TIMES if cfg.phase_times else 0) | \
-        (_lib.HJB_FLAG_GATHER_ROOT if cfg.gather_root else 0)
+        (_lib.HJB_FLAG_GATHER_ROOT if cfg.gather_root else 0) | \
+        (_lib.HJB_FLAG_VARIANT_B if cfg.variant in ("2B", "3B") else 0)
     pr.first_sweep = cfg.first_sweep
     pr.sweep_count = cfg.sweep_count
     return pr
@@ -98,8 +123,6 @@ def parallel_jacobi(G, signs, config: SolverConfig):
     Raises ValueError, PivotDefinitenessError, DefinitenessError like the
     reference.
     """
-    if config.variant not in SUPPORTED_VARIANTS:
-        raise ValueError(f"variant {config.variant!r} is not on the B200 path (2F only)")
     L = _lib.lib()
     res = _lib.Result()
     if _device.is_cuda_tensor(G):
@@ -113,7 +136,7 @@ def parallel_jacobi(G, signs, config: SolverConfig):
                       s, dev, st)
         rc = L.hjb_solve(C.byref(pr), C.byref(res))
         _lib.check(rc, res)
-        return out, _info_from(res)
+        return out, _info_from(res, pr.p)
     A = as_matrix(G)
     m, n = A.shape
     s = as_signs(signs, n)
@@ -128,7 +151,7 @@ def parallel_jacobi(G, signs, config: SolverConfig):
                   dev, None)
     rc = L.hjb_solve(C.byref(pr), C.byref(res))
     _lib.check(rc, res)
-    return out, _info_from(res)
+    return out, _info_from(res, pr.p)
 
 
 def solve_device(Gd, signs_np, config: SolverConfig, out=None, stream=None):

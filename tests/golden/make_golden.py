@@ -192,6 +192,56 @@ def fullsize():
         print(key, info.sweeps, info.rotations, f"{wall:.1f}s", f"kappa {kappa:.3e}", flush=True)
 
 
+def variants():
+    """The other reference variants on small seeded inputs: 3F / 2B / 3B
+    through parallel_jacobi (parallel.py:150-174) and the sequential drivers
+    seq / seqF / seqB through run_solver (solve.py:44-64).  Stored: the input,
+    lambda = J ||g||^2 per column of G_out, DiagInfo, kappa(G_s)."""
+    from hjacobi.factorization import scaled_condition
+    from hjacobi.solve import SolveOptions, run_solver
+    rng = np.random.default_rng(777)
+    specs = [
+        # (m, n, n_neg, complex, graded, p, strategy, variants)
+        (256, 256, 96, False, False, 4, "round_robin", ("2F", "3F", "2B", "3B")),
+        (256, 192, 64, True, False, 3, "modulus", ("2F", "3F", "2B", "3B")),
+        (256, 256, 77, False, True, 2, "round_robin", ("3F", "2B", "3B")),
+        (160, 128, 40, True, False, 2, "round_robin", ("2B", "3F")),
+        (100, 90, 33, False, False, 3, "modulus", ("2B", "3B")),     # ragged blocks of 15
+    ]
+    out, meta = {}, {}
+    for k, (m, n, nneg, cplx, graded, p, strat, vs) in enumerate(specs):
+        G = random_full_rank(rng, m, n, cplx)
+        if graded:
+            G = np.asfortranarray(G * 10.0 ** (-rng.uniform(0, 6, n)))
+        J = np.array([1] * (n - nneg) + [-1] * nneg, np.int8)
+        out[f"v{k}_G"], out[f"v{k}_J"] = G, J
+        kappa = float(np.sqrt(scaled_condition(gram(G))))
+        meta[f"v{k}"] = dict(m=m, n=n, p=p, strategy=strat, variants=list(vs), kappa=kappa, orth_tol=n * EPS)
+        for v in vs:
+            Gout, info = parallel_jacobi(G.copy(order="F"), J.copy(),
+                                         SolverConfig(variant=v, strategy=strat, p=p,
+                                                      tol=Tolerances(orth_tol=n * EPS)))
+            out[f"v{k}_{v}_lam"] = J * column_norms_squared(Gout)
+            out[f"v{k}_{v}_info"] = np.array([info.sweeps, info.rotations, info.big_rotations,
+                                             info.max_abs_t, int(info.converged)], np.float64)
+            print(f"v{k}", v, info.sweeps, info.rotations, info.converged, flush=True)
+    # sequential drivers
+    G = random_full_rank(rng, 128, 128, False)
+    J = np.array([1] * 80 + [-1] * 48, np.int8)
+    out["s_G"], out["s_J"] = G, J
+    meta["s"] = dict(n=128, nt_outer=32, kappa=float(np.sqrt(scaled_condition(gram(G)))), orth_tol=128 * EPS)
+    for v in ("seq", "seqF", "seqB"):
+        Gout, info = run_solver(G.copy(order="F"), J.copy(),
+                                SolveOptions(variant=v, nt_outer=32, tol=Tolerances(orth_tol=128 * EPS)))
+        out[f"s_{v}_lam"] = J * column_norms_squared(Gout)
+        out[f"s_{v}_info"] = np.array([info.sweeps, info.rotations, info.big_rotations,
+                                       info.max_abs_t, int(info.converged)], np.float64)
+        print("s", v, info.sweeps, info.rotations, info.converged, flush=True)
+    np.savez_compressed(os.path.join(HERE, "variants.npz"), **out)
+    with open(os.path.join(HERE, "variants.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
 def kernels():
     """Pivot-level pins: structured Cholesky and jacobi_diagonalize."""
     out = {}

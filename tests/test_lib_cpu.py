@@ -74,8 +74,12 @@ def test_validation_errors_match_reference():
         P.parallel_jacobi(G, J, P.SolverConfig(variant="2F", p=3))
     with pytest.raises(ValueError):
         P.parallel_jacobi(G, np.array([1, 2, 1, 1]), P.SolverConfig(variant="2F", p=1))
-    with pytest.raises(ValueError):  # B variants are not on the B200 path
-        P.parallel_jacobi(G, J, P.SolverConfig(variant="2B", p=1))
+    for v in ("2F", "3F", "2B", "3B"):  # every reference variant is accepted (parallel.py:43)
+        assert P.SolverConfig(variant=v).variant == v
+    assert P.SolveOptions().variant == "seq"  # the reference's default (solve.py:31)
+    from paper_1008_4166_b200.parallel import effective_p
+    assert effective_p(256, 1) == 1 and effective_p(257, 1) == 2 and effective_p(32768, 128) == 128
+    assert effective_p(600, 1) == 3 and effective_p(600, 5) == 5
 
 
 def test_uniform_partition_matches_reference_rule():

@@ -103,3 +103,22 @@ def test_reference_error_behaviour_recorded():
     G[:, 3] = 0.0
     with pytest.raises(O.CholeskyFailure):
         O.parallel_jacobi_2f(G, np.ones(16, np.int8), 2, "modulus")
+
+
+def test_oracle_2b_matches_reference_variants():
+    """The 2B restatement (oracle.parallel_jacobi_2b; parallel.py:160-174,
+    199-200) against the reference's own 2B runs (tests/golden/variants.npz):
+    same sweeps and rotation counts, eigenvalues to rounding."""
+    import json
+    z = np.load(os.path.join(GOLDEN, "variants.npz"))
+    meta = json.load(open(os.path.join(GOLDEN, "variants.json")))
+    for key in ("v0", "v1", "v3", "v4"):
+        mt = meta[key]
+        G, J = z[key + "_G"], z[key + "_J"]
+        Gout, info = O.parallel_jacobi_2b(G, J, mt["p"], mt["strategy"], orth_tol=mt["orth_tol"])
+        ref_info = z[key + "_2B_info"]
+        lam = J * O.column_norms2(Gout)
+        ref = z[key + "_2B_lam"]
+        assert info.converged and info.sweeps == int(ref_info[0]), (key, info.sweeps, ref_info)
+        assert info.rotations == int(ref_info[1]), (key, info.rotations, ref_info)
+        assert np.max(np.abs(lam - ref) / np.abs(ref)) <= 1e-12, key
