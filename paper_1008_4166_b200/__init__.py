@@ -1,7 +1,7 @@
 """B200-native hot path of the blocked one-sided hyperbolic J-Jacobi
 eigensolver (arXiv 1008.4166), drop-in for the reference package ``hjacobi``'s
-``parallel_jacobi`` / ``run_solver`` / ``solve_hermitian`` entry points with
-variant "2F".  Kernels: libhjb200.so (sm_100a); no CPU fallback.
+``parallel_jacobi`` / ``run_solver`` / ``solve_hermitian`` entry points (every
+variant).  Kernels: libhjb200.so (sm_100a); no CPU fallback.
 """
 
 from .blocking import BlockPartition, greedy_partition, num_blocks, uniform_partition
@@ -17,7 +17,9 @@ from .errors import (
     StructuralError,
 )
 from .factorization import (FactoredForm, accept_external_factor, factorize_hermitian_indefinite,
-                            order_by_inertia, scaled_condition)
+                            order_by_inertia, scaled_condition, scaled_condition_factor)
+from .matio import MatrixFormatError, read_matrix, read_matrix_pinned, read_signs, write_matrix, write_signs
+from .sequential import BlockMessage, apply_rotation, block_oriented, full_block, jacobi_diagonalize
 from .parallel import SolverConfig, parallel_jacobi
 from .rotations import (HYPERBOLIC, IDENTITY, TRIGONOMETRIC, DiagInfo, PlaneRotation, Tolerances,
                         compute_plane_rotation, extract_eigen, orthogonality)
@@ -35,4 +37,7 @@ __all__ = [
     "FactoredForm", "accept_external_factor", "factorize_hermitian_indefinite", "order_by_inertia",
     "scaled_condition", "SolveOptions", "run_solver", "solve_hermitian",
     "PlaneRotation", "compute_plane_rotation", "TRIGONOMETRIC", "HYPERBOLIC", "IDENTITY",
+    "scaled_condition_factor", "MatrixFormatError", "read_matrix", "read_matrix_pinned", "read_signs",
+    "write_matrix", "write_signs", "BlockMessage", "apply_rotation", "block_oriented", "full_block",
+    "jacobi_diagonalize",
 ]

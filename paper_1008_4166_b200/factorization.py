@@ -108,6 +108,42 @@ def scaled_condition(A):
     return math.inf if w.min() == 0.0 else float(w.max() / w.min())
 
 
+def scaled_condition_factor(G) -> float:
+    """kappa(A_s) of A = G^H G scaled to unit diagonal (factorization.py:156-168,
+    the metric of solve.py:85) WITHOUT the host n x n eigvalsh: the scaled Gram
+    is G_s^H G_s with G_s = G diag(||g_k||)^-1, so its eigenvalues are the
+    squared singular values of G_s -- the squared column norms the one-sided
+    Jacobi solver itself leaves for J = +I (all rotations trigonometric).  The
+    ring solver runs on the GPU over 64-column blocks; G may be a host array
+    or a CUDA tensor."""
+    from . import _device
+    from .parallel import SolverConfig, parallel_jacobi
+    from .rotations import Tolerances
+
+    torch = _device.torch()
+    if _device.is_cuda_tensor(G):
+        Gd = G
+    else:
+        A = as_matrix(G)
+        Gd = torch.from_numpy(np.ascontiguousarray(A.T)).to("cuda").t()
+    n = Gd.shape[1]
+    if n == 0:
+        return 1.0
+    d = (Gd.real ** 2 + Gd.imag ** 2).sum(dim=0) if Gd.is_complex() else (Gd * Gd).sum(dim=0)
+    if bool((d <= 0).any()):
+        raise ValueError("scaled_condition requires a strictly positive diagonal")
+    Gs = (Gd / torch.sqrt(d).to(Gd.dtype)[None, :]).t().contiguous().t()  # column-major
+    p = max(1, n // 128)
+    while 2 * p > n and p > 1:
+        p -= 1
+    eps = float(np.finfo(np.float64).eps)
+    cfg = SolverConfig(variant="2F", strategy="round_robin", p=p, tol=Tolerances(orth_tol=n * eps))
+    Gout, _ = parallel_jacobi(Gs, np.ones(n, np.int8), cfg)
+    w = (Gout.real ** 2 + Gout.imag ** 2).sum(dim=0) if Gout.is_complex() else (Gout * Gout).sum(dim=0)
+    lo, hi = float(w.min()), float(w.max())
+    return math.inf if lo == 0.0 else hi / lo
+
+
 def accept_external_factor(G, J) -> FactoredForm:
     """Wrap a user-supplied full-column-rank factor (factorization.py:171-189)."""
     G = as_matrix(G)

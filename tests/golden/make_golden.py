@@ -242,6 +242,20 @@ def variants():
         json.dump(meta, f, indent=1)
 
 
+def matio():
+    """HJAC files written by the reference's own writer (matio.py:26-37, 65-71)."""
+    from hjacobi.matio import write_matrix, write_signs
+    rng = np.random.default_rng(4242)
+    A = np.asfortranarray(rng.standard_normal((5, 3)))
+    Z = np.asfortranarray(rng.standard_normal((4, 6)) + 1j * rng.standard_normal((4, 6)))
+    write_matrix(os.path.join(HERE, "hjac_real.bin"), A)
+    write_matrix(os.path.join(HERE, "hjac_cplx.bin"), Z)
+    write_matrix(os.path.join(HERE, "hjac_real.txt"), A, text=True)
+    write_matrix(os.path.join(HERE, "hjac_cplx.txt"), Z, text=True)
+    write_signs(os.path.join(HERE, "hjac_signs.txt"), np.array([1, -1, 1, 1, -1, -1], np.int8))
+    np.savez(os.path.join(HERE, "hjac_expected.npz"), A=A, Z=Z)
+
+
 def kernels():
     """Pivot-level pins: structured Cholesky and jacobi_diagonalize."""
     out = {}

@@ -102,3 +102,66 @@ def test_default_options_beyond_256_columns():
     G = np.asfortranarray(rng.standard_normal((600, 600)))
     _, info = pkg.parallel_jacobi(G, np.ones(600, np.int8), pkg.SolverConfig(variant="2F", p=1))
     assert info.converged and info.stats["p_effective"] == 3
+
+
+def test_in_place_sequential_entry_points():
+    """jacobi_diagonalize / full_block / block_oriented (rotations.py:203-223,
+    blocking.py:205-293): in place, DiagInfo, W with G_in W = G_out, the
+    reference's eigenvalues."""
+    z, meta = _load()
+    mt = meta["s"]
+    J = z["s_J"]
+    tol = pkg.Tolerances(orth_tol=mt["orth_tol"])
+    bound = 64 * mt["n"] * EPS * mt["kappa"]
+    part = pkg.greedy_partition(mt["n"], mt["nt_outer"])
+    for fn, key, kw in ((lambda G: pkg.jacobi_diagonalize(G, J, tol, accumulate=True), "seq", {}),
+                        (lambda G: pkg.full_block(G, J, part, tol, accumulate_V=True), "seqF", {}),
+                        (lambda G: pkg.block_oriented(G, J, part, tol), "seqB", {})):
+        G0 = z["s_G"].copy(order="F")
+        G = G0.copy(order="F")
+        info = fn(G)
+        ref = np.sort(z[f"s_{key}_lam"])
+        got = np.sort(J * np.sum(G * G, axis=0))
+        assert info.converged and np.max(np.abs(got - ref) / np.abs(ref)) <= bound, key
+        if info.W is not None:
+            assert np.max(np.abs(G0 @ info.W - G)) <= 1e-9 * np.abs(G).max()
+            Jm = np.diag(J.astype(float))   # W is J-unitary (test_rotations.py:201-209)
+            assert np.max(np.abs(info.W.T @ Jm @ info.W - Jm)) <= 64 * mt["n"] * EPS * np.max(np.abs(info.W)) ** 2 * mt["kappa"]
+
+
+def test_apply_rotation_contract():
+    """compute_plane_rotation + apply_rotation annihilate the pivot's
+    off-diagonal Gram entry (rotations.py:128-182; test_rotations.py:41-58)."""
+    rng = np.random.default_rng(3)
+    for cx, (jr, js) in ((False, (1, 1)), (True, (1, -1)), (True, (-1, -1))):
+        G = rng.standard_normal((8, 2)) + (1j * rng.standard_normal((8, 2)) if cx else 0)
+        if jr != js:
+            G[:, 1] *= 0.3   # keep the hyperbolic pivot definite
+        A = G.conj().T @ G
+        rot = pkg.compute_plane_rotation(A[0, 0].real, A[1, 1].real, A[0, 1], jr, js)
+        D = np.array([A[0, 0].real, A[1, 1].real])
+        W = np.eye(2, dtype=G.dtype)
+        pkg.apply_rotation(G, W, D, 0, 1, rot)
+        A2 = G.conj().T @ G
+        assert abs(A2[0, 1]) <= 32 * EPS * np.sqrt(A2[0, 0].real * A2[1, 1].real)
+        assert np.allclose(D, [A2[0, 0].real, A2[1, 1].real], rtol=1e-13)
+
+
+def test_scaled_condition_on_the_gpu():
+    """kappa(A_s) from the solver itself (factorization.scaled_condition_factor)
+    equals the reference's eigvalsh-based value (factorization.py:156-168)."""
+    rng = np.random.default_rng(8)
+    for cx in (False, True):
+        G = rng.standard_normal((200, 160)) + (1j * rng.standard_normal((200, 160)) if cx else 0)
+        G = G * 10.0 ** (-rng.uniform(0, 5, 160))
+        ref = pkg.scaled_condition(G.conj().T @ G)
+        got = pkg.scaled_condition_factor(np.asfortranarray(G))
+        assert abs(got - ref) <= 1e-9 * ref, (got, ref)
+
+
+def test_read_matrix_pinned(tmp_path):
+    rng = np.random.default_rng(1)
+    Z = np.asfortranarray(rng.standard_normal((33, 7)) + 1j * rng.standard_normal((33, 7)))
+    pkg.write_matrix(tmp_path / "z.bin", Z)
+    out = pkg.read_matrix_pinned(tmp_path / "z.bin")
+    assert out.flags.f_contiguous and np.array_equal(out, Z)
