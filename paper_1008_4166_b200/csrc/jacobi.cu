@@ -601,27 +601,58 @@ __global__ void __launch_bounds__(32 * W, MINB) jacobi_kernel(JacobiArgs a) {
     }
     jb_cluster_sync<C>();
     bool bad = false;
+    // lane group g = lane >> (5 - LC) ends up with the complete dot product
+    // of local column g (butterfly reduce-scatter over the CPW partials,
+    // then a reduction inside the group): 2 CPW - 2 + (5 - LC) shuffles per
+    // column instead of 5 CPW
+    constexpr int LC = ilog2(CPW);
+    const int gc = lane >> (5 - LC);
+    double dmine = 0.0;
+    int cmine = 0;
+    bool lmine = false;
+    sfor<CPW>([&](auto cc) {
+      constexpr int c = decltype(cc)::value;
+      if (gc == c) {
+        dmine = D[c];
+        cmine = col_of(c);
+        lmine = live[c];
+      }
+    });
     for (int oc = 0; oc < Nq; ++oc) {
       T x[RPL];
 #pragma unroll
       for (int u = 0; u < RPL; ++u) x[u] = __ldcg(Rf + (lane + 32 * u) + int64_t(oc) * ld);
       const double dother = __ldcg(dsc + oc);
+      T dd[CPW];
       sfor<CPW>([&](auto cc) {
         constexpr int c = decltype(cc)::value;
-        if (live[c] && oc > col_of(c)) {  // every pair once: the owner of the lower column checks it
-          T d0 = S<T>::zero(), d1 = S<T>::zero();
+        T d0 = S<T>::zero(), d1 = S<T>::zero();
 #pragma unroll
-          for (int u = 0; u < RPL; u += 2) {
-            d0 = cfma(V[u][c], x[u], d0);
-            if (u + 1 < RPL) d1 = cfma(V[u + 1][c], x[u + 1], d1);
-          }
-          T dd = add(d0, d1);
-#pragma unroll
-          for (int dist = 16; dist >= 1; dist >>= 1) dd = add(dd, shfl_xor(dd, dist));
-          bad |= !(abs2(dd) <= otol2 * (D[c] * dother));
+        for (int u = 0; u < RPL; u += 2) {
+          d0 = cfma(V[u][c], x[u], d0);
+          if (u + 1 < RPL) d1 = cfma(V[u + 1][c], x[u + 1], d1);
         }
+        dd[c] = add(d0, d1);
       });
+#pragma unroll
+      for (int j = 0; j < LC; ++j) {
+        const int dist = 16 >> j;
+        const bool hi = lane & dist;
+        const int half = CPW >> (j + 1);
+#pragma unroll
+        for (int xx = 0; xx < half; ++xx) {
+          const T snd = hi ? dd[xx] : dd[xx + half];
+          const T keep = hi ? dd[xx + half] : dd[xx];
+          dd[xx] = add(keep, shfl_xor(snd, dist));
+        }
+      }
+      T acc = dd[0];
+#pragma unroll
+      for (int dist = 16 >> LC; dist >= 1; dist >>= 1) acc = add(acc, shfl_xor(acc, dist));
+      // every pair once: the owner of the lower column checks it
+      if (lmine && oc > cmine) bad |= !(abs2(acc) <= otol2 * (dmine * dother));
     }
+    bad = __any_sync(0xffffffffu, bad);
     if (bad && lane == 0) atomicOr(&s_chk[slot], 1);
     jb_cluster_sync<C>();
     int any_bad = 0;
