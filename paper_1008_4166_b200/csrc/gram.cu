@@ -114,6 +114,32 @@ __global__ void __launch_bounds__(GramCfg<T, WM, WN, MI, NI, KC, STAGES>::NT, MI
     }
   };
 
+  // Full tiles and whole K chunks (every BASELINE config): thread t stages
+  // pieces t, t + NT, ... whose column advances by NT / PPC per piece, so a
+  // stage is two base pointers plus compile-time strides -- no per-piece
+  // div/mod or bounds arithmetic
+  constexpr int CS = NT / PPC;  // column stride between a thread's pieces
+  constexpr bool FAST_OK = VEC == 16 && NT % PPC == 0 && TM % CS == 0 && TN % CS == 0;
+  const bool fast_cols = FAST_OK && cX == TM && cY == TN;
+  const int col0 = tid / PPC, within0 = tid % PPC;
+  const T *xsrc0 = G + int64_t(oX + col0) * a.ldg + within0 * EPP;
+  const T *ysrc0 = G + int64_t(oY + col0) * a.ldg + within0 * EPP;
+  const int64_t sstride = int64_t(CS) * a.ldg;
+  auto load_stage_fast = [&](int stage, int chunk) {
+    T *Xs = smem + stage * Cfg::STAGE_ELEMS + col0 * KCP + within0 * EPP;
+    const int64_t kb = k0 + int64_t(chunk) * KC;
+    if constexpr (FAST_OK) {
+#pragma unroll
+      for (int i = 0; i < TM / CS; ++i) cp_async16(Xs + i * CS * KCP, xsrc0 + i * sstride + kb, 16);
+#pragma unroll
+      for (int i = 0; i < TN / CS; ++i) cp_async16(Xs + (TM + i * CS) * KCP, ysrc0 + i * sstride + kb, 16);
+    }
+  };
+  auto stage_in = [&](int stage, int chunk) {
+    if (fast_cols && k0 + int64_t(chunk + 1) * KC <= k1) load_stage_fast(stage, chunk);
+    else load_stage(stage, chunk);
+  };
+
   GramAcc<T> acc[MI][NI];
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi)
@@ -129,7 +155,7 @@ __global__ void __launch_bounds__(GramCfg<T, WM, WN, MI, NI, KC, STAGES>::NT, MI
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nchunks) load_stage(s, s);
+    if (s < nchunks) stage_in(s, s);
     cp_async_commit();
   }
   for (int c = 0; c < nchunks; ++c) {
@@ -137,7 +163,7 @@ __global__ void __launch_bounds__(GramCfg<T, WM, WN, MI, NI, KC, STAGES>::NT, MI
     __syncthreads();
     {
       const int nxt = c + STAGES - 1;
-      if (nxt < nchunks) load_stage(nxt % STAGES, nxt);
+      if (nxt < nchunks) stage_in(nxt % STAGES, nxt);
       cp_async_commit();
     }
     const T *Xs = smem + (c % STAGES) * Cfg::STAGE_ELEMS;

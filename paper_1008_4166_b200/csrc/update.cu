@@ -105,16 +105,55 @@ __global__ void __launch_bounds__(256, (UpdCfg<T, NMAX, MT, KW>::MINB)) update_k
     }
   };
 
+  // Full tiles (every BASELINE config: N == NMAX, whole row tiles, K chunks
+  // inside one block): the per-thread source offsets are loop invariant, so a
+  // stage costs one address add per 16-byte piece instead of the div/mod and
+  // bounds arithmetic above
+  constexpr int XP = MT / EPP, XPT = (KW * XP + NT - 1) / NT;
+  constexpr int EW = 16 / int(sizeof(T)), WP = KW / EW, WPT = (NMAX * WP + NT - 1) / NT;
+  const bool full = VEC == 16 && N == NMAX && r0 + MT <= a.m && ni % KW == 0;
+  int64_t xoff[XPT];
+  int xdst[XPT], woff[WPT], wdst[WPT];
+#pragma unroll
+  for (int i = 0; i < XPT; ++i) {
+    const int pc = tid + i * NT, k = pc / XP, w = pc % XP;
+    xoff[i] = int64_t(k) * a.ldg + r0 + int64_t(w) * EPP;
+    xdst[i] = k * MTP + w * EPP;
+  }
+#pragma unroll
+  for (int i = 0; i < WPT; ++i) {
+    const int pc = tid + i * NT, c = pc / WP, w = pc % WP;
+    woff[i] = w * EW + c * a.nmax;
+    wdst[i] = c * KWP + w * EW;
+  }
+  auto load_stage_full = [&](int stage, int chunk) {
+    T *Xs = smem + stage * Cfg::STAGE;
+    T *Wsm = Xs + Cfg::XS;
+    const int kb = chunk * KW;
+    const T *gsrc = G + int64_t(kb < ni ? it.oi + kb : it.oj + (kb - ni)) * a.ldg;
+    const T *wsrc = W + kb;
+#pragma unroll
+    for (int i = 0; i < XPT; ++i)
+      if ((KW * XP) % NT == 0 || tid + i * NT < KW * XP) cp_async16(Xs + xdst[i], gsrc + xoff[i], 16);
+#pragma unroll
+    for (int i = 0; i < WPT; ++i)
+      if ((NMAX * WP) % NT == 0 || tid + i * NT < NMAX * WP) cp_async16(Wsm + wdst[i], wsrc + woff[i], 16);
+  };
+  auto stage_in = [&](int stage, int chunk) {
+    if (full) load_stage_full(stage, chunk);
+    else load_stage(stage, chunk);
+  };
+
   UpdAcc<T> acc[MI][NI];
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
     for (int nn = 0; nn < NI; ++nn) acc[mi][nn].zero();
 
-  load_stage(0, 0);
+  stage_in(0, 0);
   cp_async_commit();
   for (int c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) load_stage((c + 1) & 1, c + 1);
+    if (c + 1 < nchunks) stage_in((c + 1) & 1, c + 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
