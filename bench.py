@@ -28,9 +28,16 @@ p worker threads coupled through ring channels) on the host cores.
 
 from __future__ import annotations
 
+import os
+
+# The reference pins BLAS to one thread per ring worker; this
+# must be in the environment BEFORE numpy loads OpenBLAS, or the p worker
+# threads of the CPU baseline oversubscribe the cores (measured: cfg1 7.0 s
+# instead of 1.8 s).
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
 import argparse
 import json
-import os
 import platform
 import statistics
 import subprocess
@@ -185,27 +192,42 @@ def cpu_profile():
 def cpu_sample(w, full):
     """The reference's algorithm on the host (oracle restatement pinned
     bit-exact to the reference).  full=True: one whole solve, run as the
-    reference runs it (p worker threads on ring channels).  full=False: the
-    first F pre-pass and the first ring step of sweep 1 (p pairs, p threads),
-    extrapolated to the whole solve with the cost profile of the reference
-    algorithm on the same-generator proxy measured in the build container
-    (oracle/cpu_profile.json) -- an ESTIMATE, labelled as one."""
+    reference runs it (p worker threads on ring channels).  full=False: a
+    bounded sample extrapolated to the whole solve, labelled an ESTIMATE:
+    cfg2 / cfg3 -- the first outer sweep, times the whole-solve / first-sweep
+    ratio of the reference algorithm measured in the build container
+    (oracle/cpu_profile.json, cfg2: 59.0 s / 8.9 s over 14 sweeps, scaled by
+    the sweep count for cfg3); cfg4 / cfg5 -- the first F pre-pass and the
+    first ring step of sweep 1 (p pairs, p threads), times the cost profile of
+    the same-generator proxy (SURVEY.md 8(d) item iv)."""
     import oracle
     threads = w.p
     oracle.parallel_jacobi_2f(w.G[:128, :128], w.J[:128], 2, "round_robin", orth_tol=w.orth_tol)  # JIT warm
+    prof = cpu_profile()
     t0 = time.perf_counter()
     if full:
         _, info = oracle.parallel_jacobi_2f(w.G, w.J, w.p, "round_robin", orth_tol=w.orth_tol, threads="ring")
         t = time.perf_counter() - t0
         return t, t, f"one whole {w.name} solve ({info.sweeps} sweeps), p={w.p} ring worker threads"
+    if w.name in ("cfg2", "cfg3"):
+        _, info = oracle.parallel_jacobi_2f(w.G, w.J, w.p, "round_robin", orth_tol=w.orth_tol, threads=threads,
+                                            sweep_limit=1)
+        t = time.perf_counter() - t0
+        c2 = prof.get("cfg2", {})
+        ratio = c2.get("t_total", 59.0) / c2.get("t_sweep1", 8.86)
+        sweeps_ref = {"cfg2": 14, "cfg3": 15}[w.name]
+        factor = ratio * sweeps_ref / 14.0
+        return t, t * factor, (f"first outer sweep of {w.name} ({threads} threads), {t:.2f} s; whole-solve ESTIMATE "
+                               f"x{factor:.2f} (whole/first-sweep ratio of the cfg2 reference run, "
+                               f"{sweeps_ref} sweeps)")
     _, info = oracle.parallel_jacobi_2f(w.G, w.J, w.p, "round_robin", orth_tol=w.orth_tol, threads=threads,
                                         sweep_limit=1, step_limit=1)
     t = time.perf_counter() - t0
-    prof = cpu_profile().get(w.name + "_extrapolation", {})
-    factor = prof.get("factor")
+    ex = prof.get(w.name + "_extrapolation", {})
+    factor = ex.get("factor")
     est = t * factor if factor else None
     desc = (f"F pre-pass + first ring step of sweep 1 of {w.name} ({w.p} pairs, {threads} threads), "
-            f"{t:.2f} s; whole-solve ESTIMATE x{factor:.0f} ({prof.get('how', '')})" if factor else
+            f"{t:.2f} s; whole-solve ESTIMATE x{factor:.0f} ({ex.get('how', '')})" if factor else
             f"F pre-pass + first ring step of sweep 1 ({t:.2f} s), no extrapolation profile")
     return t, est, desc
 
@@ -215,7 +237,7 @@ def reference_arm(args, w):
     if rank != 0:
         return
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    full = w.name not in SWEEP_STEP_CONFIGS and w.name != "cfg3"
+    full = w.name == "cfg1"   # the others: bounded samples (cpu_sample), so K steps end within minutes
     cores = os.cpu_count() or 1
     for _ in range(max(0, min(args.warmup, 1))):
         cpu_sample(w, full)
@@ -456,9 +478,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-        t, est, desc = cpu_sample(w, full=False)
+        t, est, desc = cpu_sample(w, full=w.name == "cfg1")
         cpu = {"value": est if est else t, "unit": "s", "cores": min(os.cpu_count() or 1, w.p), "kind": "port",
-               "sample": desc, "cpu_model": cpu_model(), "nproc": os.cpu_count(), "extrapolated": True}
+               "sample": desc, "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+               "extrapolated": w.name != "cfg1"}
     if rank == 0:
         step_desc = ("one outer sweep of the solve (value = first complete solve in the timed region"
                      + ("" if finished_inside else ", finished after the timed region") + ")") \

@@ -206,8 +206,10 @@ int hjb_pivot_ld(int32_t bmax);
  * round-1 pivot kernel, per warp [count*C*W][8] for the Jacobi kernel
  * (builds with -DHJB_JAC_PROF=1). */
 int hjb_pivot_set_profile(void *prof);
-/* Tuning override for the pivot kernel: threads per CTA (256/512/1024) and
- * cluster size (1..16); 0 restores the automatic choice. */
+/* Tuning override (experiments): threads per CTA of the round-1 pivot kernel
+ * (128/256/512, the instantiated shapes) and the cluster size (1..16) of the
+ * pivot / Jacobi kernel; 0 restores the automatic choice.  An unsupported
+ * combination makes the next launch fail with "invalid configuration". */
 int hjb_tune(int32_t pivot_threads, int32_t pivot_cluster);
 /* Inner pair order of hjb_pivot for (dtype, bmax, count, cluster; 0 = auto):
  * the warp-block order over *nmax column positions in *warps warps per CTA
