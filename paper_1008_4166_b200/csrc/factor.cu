@@ -197,6 +197,9 @@ __global__ void __launch_bounds__(ProCfg<T, B>::NT, 1) factor_prologue_kernel(Pi
     if (!dense && c >= B && c - B < nj) v = a.D[int64_t(item_id) * 2 * bmax + bmax + (c - B)];
     lam[c] = v;
   }
+  // R0 is zero outside the pieces written below (strict lower triangle,
+  // padding up to nmax): store-only, overlaps with everything that follows
+  for (int e = tid; e < ld * ld; e += NT) R0[e] = S<T>::zero();
   __syncthreads();
   int status = PV_OK, fallback = 0;
   bool structured = false;
@@ -214,10 +217,18 @@ __global__ void __launch_bounds__(ProCfg<T, B>::NT, 1) factor_prologue_kernel(Pi
       constexpr int TJ = B / 32, NTILE = (B / 16) * TJ;  // 16 x 32 tiles
       for (int h0 = 0; h0 < ni; h0 += KC) {
         __syncthreads();
+        // stage R_ij = A_ij / sqrt(L_i) (rows h0 .. h0 + KC) and write it to
+        // its place in R0 on the way (the top-right block)
+#pragma unroll 4
         for (int e = tid; e < B * KC; e += NT) {
           const int k = e % KC, l = e / KC;
           const int h = h0 + k;
-          Xs[l * KCP + k] = (h < ni && l < nj) ? divr(A[h + int64_t(l) * bmax], sq[h]) : S<T>::zero();
+          T v = S<T>::zero();
+          if (h < ni && l < nj) {
+            v = divr(A[h + int64_t(l) * bmax], sq[h]);
+            R0[h + int64_t(ni + l) * ld] = v;
+          }
+          Xs[l * KCP + k] = v;
         }
         __syncthreads();
         for (int t = warp; t < NTILE; t += NW) {
@@ -309,18 +320,14 @@ __global__ void __launch_bounds__(ProCfg<T, B>::NT, 1) factor_prologue_kernel(Pi
       __syncthreads();
     }
   } else if (status == PV_OK) {
-    // R0 (nmax x nmax, zero padded) -> global for the Jacobi kernel and the epilogue
-    const int nt = dense ? 0 : ni;  // rows with the diagonal sqrt(L_i) block
-    for (int e = tid; e < ld * ld; e += NT) {
-      const int g = e % ld, c = e / ld;
-      T v = S<T>::zero();
-      if (g < N && c < N && c >= g) {
-        if (g < nt)
-          v = c == g ? scale(S<T>::one(), sq[g]) : (c < nt ? S<T>::zero() : divr(A[g + int64_t(c - nt) * bmax], sq[g]));
-        else
-          v = Sp[pk(g - nt, c - nt)];
-      }
-      R0[e] = v;
+    // the rest of R0 (zero filled above, R_ij written while staging): the
+    // diagonal sqrt(L_i) block and the Cholesky factor of the second block
+    const int nt = dense ? 0 : ni;
+    for (int g = tid; g < nt; g += NT) R0[g + int64_t(g) * ld] = scale(S<T>::one(), sq[g]);
+    const int nu2 = N - nt;
+    for (int e = tid; e < nu2 * nu2; e += NT) {
+      const int g = e % nu2, c = e / nu2;
+      if (g <= c) R0[(nt + g) + int64_t(nt + c) * ld] = Sp[pk(g, c)];
     }
   }
   if (tid == 0) {
@@ -569,6 +576,14 @@ __global__ void __launch_bounds__(256) factor_epilogue_kernel(PivotArgs a) {
   for (int I = nblk - 1; I >= 0; --I) {
     const int r0 = 32 * I;
     // ---- T_I = F_I - R0[I, k] W[k, :] over the rows below the block ----
+    // the diagonal block's row of this lane and its reciprocal pivot: loaded
+    // first so that their L2 latency overlaps the DMMA part
+    const int row = r0 + lane;
+    T rr[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      rr[r] = (r > lane && row < N && r0 + r < N) ? __ldcg(R0 + row + int64_t(r0 + r) * ld) : S<T>::zero();
+    const double rdiag = row < N ? re(__ldcg(R0 + row + int64_t(row) * ld)) : 1.0;
     int kstart = r0 + 32;
     if (structured && r0 + 32 <= ni) kstart = max(kstart, ni & ~3);  // the sqrt(L_i) block is diagonal
     if (kstart < kend) {
@@ -596,12 +611,7 @@ __global__ void __launch_bounds__(256) factor_epilogue_kernel(PivotArgs a) {
     // ---- W_I = R0[I, I]^-1 T_I: lane s holds row r0 + s; each solved row is
     // broadcast by a shuffle (the diagonal of a Cholesky factor is real) ----
     {
-      const int row = r0 + lane;
-      T rr[32];
-#pragma unroll
-      for (int r = 0; r < 32; ++r)
-        rr[r] = (r > lane && row < N && r0 + r < N) ? __ldcg(R0 + row + int64_t(r0 + r) * ld) : S<T>::zero();
-      const double rinv = row < N ? 1.0 / re(__ldcg(R0 + row + int64_t(row) * ld)) : 0.0;
+      const double rinv = row < N ? 1.0 / rdiag : 0.0;
       T t[CPW];
 #pragma unroll
       for (int j = 0; j < CPW; ++j) t[j] = Fs[(warp * CPW + j) * LDF + row];

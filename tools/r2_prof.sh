@@ -17,10 +17,10 @@ export_rep() {
   gzip -f $1_raw.csv $1_jac_sass.csv
   rm -f $1.ncu-rep
 }
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"jacobi_kernel|update_kernel|gram_kernel|pivot_kernel" -s 12 -c 5 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"jacobi_kernel|update_kernel|gram_kernel|gram_reduce|factor_" -s 14 -c 7 \
   -o /tmp/full_cfg5r_$T python tools/profile_solve.py cfg5r --sweeps 1 > $O/ncu_f5_$T.log 2>&1
 export_rep /tmp/full_cfg5r_$T; mv /tmp/full_cfg5r_${T}_* $O/
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"jacobi_kernel|pivot_kernel|gram_kernel|update_kernel" -s 20 -c 5 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"jacobi_kernel|factor_|gram_kernel|gram_reduce|update_kernel" -s 24 -c 7 \
   -o /tmp/full_cfg2_$T python tools/profile_solve.py cfg2 > $O/ncu_f2_$T.log 2>&1
 export_rep /tmp/full_cfg2_$T; mv /tmp/full_cfg2_${T}_* $O/
 du -sh $O
