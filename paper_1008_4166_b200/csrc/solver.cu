@@ -119,15 +119,19 @@ Partition uniform_partition(int64_t n, int nbl) {  // blocking.py:63-68
   return P;
 }
 
-// Inner level: the ring-of-rings Jacobi kernel between the pivot kernel's
-// prologue and epilogue (default), or the round-1 single pivot kernel
-// (HJB_PIVOT_V1=1, kept for A/B measurements).
-bool inner_v1() {
-  static const bool v1 = [] {
+// Inner level: the factor prologue, the ring-of-rings Jacobi kernel and the
+// factor epilogue (three launches), or the single cluster pivot kernel of
+// round 1 (one launch).  Measured (profiles/r2_inner_v1_ab.jsonl): the three
+// kernels win for pivots of order 128 and 256 (cfg2 396 vs 433 ms, cfg3 629
+// vs 674 ms), the single launch for order <= 64 (cfg1 54.6 vs 61.6 ms), where
+// a pivot is too small to amortise two more launches.  HJB_PIVOT_V1=1 / =0
+// forces one or the other (A/B runs).
+bool inner_v1(int nmax) {
+  static const int forced = [] {
     const char *e = std::getenv("HJB_PIVOT_V1");
-    return e && std::atoi(e) != 0;
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : -1;
   }();
-  return v1;
+  return forced >= 0 ? forced == 1 : nmax <= 64;
 }
 
 // round-1 prologue / epilogue inside the cluster pivot kernel (HJB_FACTOR_V1=1, A/B only)
@@ -143,7 +147,7 @@ bool factor_v1() {
 cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st, int *cluster_used, int *launches,
                          int jac_mode = JAC_CONVERGE) {
   const bool vb = pa.fp_input == FP_DENSE_PAIR;  // B variants: always the round-2 kernels
-  if (inner_v1() && !vb) {
+  if (inner_v1(pa.nmax) && !vb) {
     pa.mode = PV_FULL;
     ++*launches;
     return launch_pivot(cx, pa, cluster_req, st, cluster_used);
@@ -433,7 +437,7 @@ int hjb_inner_order(int32_t dtype, int32_t bmax, int32_t count, int32_t cluster,
   const bool cx = dtype == HJB_C128;
   const int nm = pivot_nmax(bmax);
   if (nm < 0 || count < 1 || !desc) return fail(HJB_EINVAL, "hjb_inner_order: bad arguments");
-  if (inner_v1()) {
+  if (inner_v1(nm)) {
     const int c = cluster > 0 ? cluster : pivot_choose_cluster(cx, nm, count);
     desc[0] = 1;
     desc[1] = nm;
