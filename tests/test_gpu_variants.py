@@ -165,3 +165,39 @@ def test_read_matrix_pinned(tmp_path):
     pkg.write_matrix(tmp_path / "z.bin", Z)
     out = pkg.read_matrix_pinned(tmp_path / "z.bin")
     assert out.flags.f_contiguous and np.array_equal(out, Z)
+
+
+@pytest.mark.parametrize("cx", [False, True], ids=["f64", "c128"])
+@pytest.mark.parametrize("n,m,p,variant,strategy", [
+    (96, 100, 3, "2F", "round_robin"),    # b = 16: the order-32 pivot instance, m > n
+    (130, 131, 2, "2F", "round_robin"),   # ragged blocks 33/33/32/32 -> order-128 instance, odd m
+    (260, 260, 2, "2F", "modulus"),       # b = 65 -> order-256 instance with padding
+    (130, 131, 2, "2B", "round_robin"),
+    (260, 260, 2, "2B", "round_robin"),
+    (96, 100, 3, "2B", "modulus"),
+])
+def test_ragged_shapes_every_kernel_instance(cx, n, m, p, variant, strategy):
+    """Odd row counts, ragged and padded blocks through every pivot-order
+    instance of the factor / Jacobi / update kernels, both variants, against
+    the oracle's restatement of the same variant."""
+    import oracle as O
+    rng = np.random.default_rng(n + m + p)
+    G = rng.standard_normal((m, n)) + (1j * rng.standard_normal((m, n)) if cx else 0)
+    G = np.asfortranarray(G)
+    J = np.array([1] * (n - n // 3) + [-1] * (n // 3), np.int8)
+    tol = n * EPS
+    if variant == "2F":
+        ref_G, ref_info = O.parallel_jacobi_2f(G, J, p, strategy, orth_tol=tol)
+    else:
+        ref_G, ref_info = O.parallel_jacobi_2b(G, J, p, strategy, orth_tol=tol)
+    Gout, info = pkg.parallel_jacobi(G, J, pkg.SolverConfig(variant=variant, strategy=strategy, p=p,
+                                                           tol=pkg.Tolerances(orth_tol=tol)))
+    ref = np.sort(J * O.column_norms2(ref_G))
+    got = np.sort(J * np.sum(np.abs(np.asarray(Gout)) ** 2, axis=0))
+    kappa = np.sqrt(O.scaled_condition(O.gram(G)))
+    assert info.converged and abs(info.sweeps - ref_info.sweeps) <= (1 if variant == "2F" else 2)
+    assert np.max(np.abs(got - ref) / np.abs(ref)) <= 64 * n * EPS * kappa
+    # column order is preserved (parallel.py:299-301): every output column keeps its sign's inertia count
+    res = pkg.extract_eigen(Gout, J)
+    lam = res.eigenvalues.cpu().numpy() if hasattr(res.eigenvalues, "cpu") else np.asarray(res.eigenvalues)
+    assert np.all(np.sign(lam) == J)
