@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.environ.get("HJB_LIB") or os.path.join(HERE, "libhjb200.so")
 OBJ = os.path.join(ROOT, "build", "obj" + os.environ.get("HJB_OBJ_TAG", ""))
-SOURCES = ["schedule.cpp", "gram.cu", "pivot.cu", "factor.cu", "jacobi.cu", "update.cu", "solver.cu"]
+SOURCES = ["schedule.cpp", "gram.cu", "pivot.cu", "pivot_c128.cu", "factor.cu", "jacobi.cu", "update.cu", "solver.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -53,7 +53,8 @@ def _up_to_date(src, obj, flags):
     if open(stamp).read() != " ".join(flags):
         return False
     t = os.path.getmtime(obj)
-    return all(os.path.getmtime(d) <= t for d in [src] + HEADERS if os.path.exists(d))
+    deps = [src] + HEADERS + ([os.path.join(CSRC, "pivot.cu")] if src.endswith("pivot_c128.cu") else [])
+    return all(os.path.getmtime(d) <= t for d in deps if os.path.exists(d))
 
 
 def _compile(src, inc, verbose, force=False):

@@ -62,7 +62,13 @@ namespace cg = cooperative_groups;
 namespace hjb {
 
 constexpr double kEps = 2.220446049250313e-16;
+// This file builds as TWO translation units to halve the wall time of the
+// library build: pivot.cu itself (the float64 instantiations and every
+// non-template function) and pivot_c128.cu, which defines HJB_PIVOT_CPLX_TU
+// and includes this file (the complex128 instantiations only).
+#ifndef HJB_PIVOT_CPLX_TU
 static int g_tune_threads = 0, g_tune_cluster = 0;  // hjb_tune overrides (0 = auto)
+#endif
 
 template <typename T, int NMAX, int C, int NT>
 struct PivCfg {
@@ -221,6 +227,7 @@ __global__ void plane_rotation_kernel(int count, const double *arr, const double
   o[7] = p.hyp;
 }
 
+#ifndef HJB_PIVOT_CPLX_TU
 cudaError_t launch_plane_rotations(bool cx, int count, const double *arr, const double *ass, const void *ars,
                                    const int8_t *same, double *out, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
@@ -231,6 +238,7 @@ cudaError_t launch_plane_rotations(bool cx, int count, const double *arr, const 
     plane_rotation_kernel<double><<<nb, 128, 0, st>>>(count, arr, ass, static_cast<const double *>(ars), same, out);
   return cudaGetLastError();
 }
+#endif  // !HJB_PIVOT_CPLX_TU
 
 template <typename T, int NMAX, int C, int NT>
 __global__ void __launch_bounds__(NT, 1) pivot_kernel(PivotArgs a) {
@@ -1452,6 +1460,7 @@ static cudaError_t launch_pivot_t(const PivotArgs &a, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, k, a);
 }
 
+#ifndef HJB_PIVOT_CPLX_TU
 size_t pivot_check_elems(int nmax) {
   const size_t nb = nmax / 4;
   return 16 * (nb * (nb + 1) / 2) * 16;  // up to 16 CTAs per cluster
@@ -1498,7 +1507,14 @@ int pivot_default_cluster(bool cx, int nmax, int count) {
   return best;
 }
 
-static int g_query_clusters = 0;  // when set, launch_pivot only reports max active clusters
+#endif  // !HJB_PIVOT_CPLX_TU
+
+// when set, launch_pivot only reports max active clusters
+#ifdef HJB_PIVOT_CPLX_TU
+extern int g_query_clusters;
+#else
+int g_query_clusters = 0;
+#endif
 
 template <typename T, int NMAX, int C, int NT>
 static cudaError_t query_clusters(int *out) {
@@ -1553,6 +1569,7 @@ static cudaError_t launch_if_valid(const PivotArgs &a, cudaStream_t st) {
   return cudaErrorInvalidConfiguration;
 }
 
+#ifndef HJB_PIVOT_CPLX_TU
 int pivot_max_active_clusters(bool cx, int nmax, int c, int nt) {
   g_query_clusters = 1;
   PivotArgs a{};
@@ -1567,6 +1584,7 @@ int pivot_max_active_clusters(bool cx, int nmax, int c, int nt) {
   g_query_clusters = 0;
   return e == cudaSuccess ? r : -int(e);
 }
+#endif  // !HJB_PIVOT_CPLX_TU
 
 template <typename T, int NMAX, int C>
 static cudaError_t dispatch_nt(const PivotArgs &a, int nt, cudaStream_t st) {
@@ -1589,6 +1607,19 @@ static cudaError_t dispatch_c(const PivotArgs &a, int c, int nt, cudaStream_t st
   }
   return cudaErrorInvalidConfiguration;
 }
+
+#ifdef HJB_PIVOT_CPLX_TU
+cudaError_t launch_pivot_cplx(const PivotArgs &a, int c, int nt, cudaStream_t st) {
+  switch (a.nmax) {
+    case 32: return dispatch_c<cplx, 32>(a, c, nt, st);
+    case 64: return dispatch_c<cplx, 64>(a, c, nt, st);
+    case 128: return dispatch_c<cplx, 128>(a, c, nt, st);
+    case 256: return dispatch_c<cplx, 256>(a, c, nt, st);
+  }
+  return cudaErrorInvalidValue;
+}
+#else
+cudaError_t launch_pivot_cplx(const PivotArgs &a, int c, int nt, cudaStream_t st);  // pivot_c128.cu
 
 void pivot_tune(int threads, int cluster) {
   g_tune_threads = threads;
@@ -1619,22 +1650,15 @@ cudaError_t launch_pivot(bool cx, const PivotArgs &a, int cluster, cudaStream_t 
   int c = cluster > 0 ? cluster : (g_tune_cluster > 0 ? g_tune_cluster : pivot_default_cluster(cx, a.nmax, a.count));
   const int nt = g_tune_threads > 0 ? g_tune_threads : pivot_default_threads(cx, a.nmax, c);
   if (cluster_used) *cluster_used = c;
-  if (cx) {
-    switch (a.nmax) {
-      case 32: return dispatch_c<cplx, 32>(a, c, nt, st);
-      case 64: return dispatch_c<cplx, 64>(a, c, nt, st);
-      case 128: return dispatch_c<cplx, 128>(a, c, nt, st);
-      case 256: return dispatch_c<cplx, 256>(a, c, nt, st);
-    }
-  } else {
-    switch (a.nmax) {
-      case 32: return dispatch_c<double, 32>(a, c, nt, st);
-      case 64: return dispatch_c<double, 64>(a, c, nt, st);
-      case 128: return dispatch_c<double, 128>(a, c, nt, st);
-      case 256: return dispatch_c<double, 256>(a, c, nt, st);
-    }
+  if (cx) return launch_pivot_cplx(a, c, nt, st);
+  switch (a.nmax) {
+    case 32: return dispatch_c<double, 32>(a, c, nt, st);
+    case 64: return dispatch_c<double, 64>(a, c, nt, st);
+    case 128: return dispatch_c<double, 128>(a, c, nt, st);
+    case 256: return dispatch_c<double, 256>(a, c, nt, st);
   }
   return cudaErrorInvalidValue;
 }
+#endif  // HJB_PIVOT_CPLX_TU
 
 }  // namespace hjb
