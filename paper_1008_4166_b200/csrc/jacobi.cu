@@ -874,4 +874,57 @@ cudaError_t launch_jacobi(bool cx, const JacobiArgs &a, JacShape s, cudaStream_t
   return cx ? dispatch_jacobi<cplx>(a, s, st) : dispatch_jacobi<double>(a, s, st);
 }
 
+// Pivots (clusters) of this shape that are resident on the GPU at once: one
+// "wave" of the Jacobi launch (cudaOccupancyMaxActiveClusters, cached).
+template <typename T, int N, int C, int W, int SPW>
+static int query_jacobi_t() {
+  using Cfg = JacCfg<T, N, C, W, SPW>;
+  constexpr int MINB = Cfg::NT <= 128 ? 2 : 1;
+  auto k = jacobi_kernel<T, N, C, W, SPW, MINB>;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)) != cudaSuccess) return 0;
+  if (C > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * 256);
+  cfg.blockDim = dim3(Cfg::NT);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = C;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+template <typename T>
+static int query_jacobi(int nmax, JacShape s) {
+#define HJB_JAC_Q(N_, C_, W_, S_)                  \
+  if constexpr (jac_shape_ok<T, N_, S_>())          \
+    if (nmax == N_ && s.c == C_ && s.w == W_ && s.spw == S_) return query_jacobi_t<T, N_, C_, W_, S_>();
+  HJB_JAC_SHAPES(HJB_JAC_Q)
+#undef HJB_JAC_Q
+  return 0;
+}
+
+int jacobi_wave_capacity(bool cx, int nmax, JacShape s) {
+  static int cache[64][2][4][5];  // [device][type][nmax][log2 cluster]
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  const int ni = nmax == 32 ? 0 : nmax == 64 ? 1 : nmax == 128 ? 2 : 3;
+  int ci = 0;
+  while ((1 << ci) < s.c && ci < 4) ++ci;
+  int &v = cache[dev][cx][ni][ci];
+  if (v == 0) {
+    v = cx ? query_jacobi<cplx>(nmax, s) : query_jacobi<double>(nmax, s);
+    if (v <= 0) v = -1;
+  }
+  return v > 0 ? v : 0;
+}
+
 }  // namespace hjb

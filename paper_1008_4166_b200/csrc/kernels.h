@@ -91,6 +91,7 @@ struct JacShape {
 JacShape jacobi_default_shape(bool cx, int nmax, int count);
 bool jacobi_shape_for(int nmax, int c, JacShape *out);  // an instantiated shape with cluster size c
 cudaError_t launch_jacobi(bool cx, const JacobiArgs &a, JacShape s, cudaStream_t st);
+int jacobi_wave_capacity(bool cx, int nmax, JacShape s);  // clusters resident at once (0: unknown)
 
 struct UpdateArgs {
   void *G;

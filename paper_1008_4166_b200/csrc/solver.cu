@@ -85,6 +85,8 @@ struct Workspace {
   DBuf G, items, gitems, A, D, W, U, Gc, R0, Dc, Gp, stats, signs, red, lam, flag;
   HBuf stats_h, red_h;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // tail split of the Jacobi launch (run_phase)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> events;
 };
 
@@ -143,20 +145,7 @@ bool factor_v1() {
   return v1;
 }
 
-// the three pivot-phase launches of one batch (or the single v1 launch)
-cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st, int *cluster_used, int *launches,
-                         int jac_mode = JAC_CONVERGE) {
-  const bool vb = pa.fp_input == FP_DENSE_PAIR;  // B variants: always the round-2 kernels
-  if (inner_v1(pa.nmax) && !vb) {
-    pa.mode = PV_FULL;
-    ++*launches;
-    return launch_pivot(cx, pa, cluster_req, st, cluster_used);
-  }
-  long long *prof = pa.prof;  // phase clocks are the Jacobi kernel's
-  pa.prof = nullptr;
-  pa.mode = PV_PROLOGUE;
-  cudaError_t e = (factor_v1() && !vb) ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_prologue(cx, pa, st);
-  if (e != cudaSuccess) return e;
+JacobiArgs jacobi_args(const PivotArgs &pa, int jac_mode) {
   JacobiArgs j{};
   j.items = pa.items;
   j.count = pa.count;
@@ -169,13 +158,31 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   j.quad_tol = pa.quad_tol;
   j.max_sweeps = pa.max_sweeps;
   j.stats = pa.stats;
-  j.prof = prof;
+  j.prof = pa.prof;  // phase clocks are the Jacobi kernel's
   static const bool nocheck = [] {  // A/B only: run the final zero-rotation sweep instead of the Gram check
     const char *e = std::getenv("HJB_JAC_NOCHECK");
     return e && std::atoi(e) != 0;
   }();
   j.dscr = nocheck ? nullptr : static_cast<double *>(pa.dscr);
   j.mode = jac_mode;
+  return j;
+}
+
+// the pivot-phase launches of one batch: factor prologue, Jacobi, factor
+// epilogue (or the single v1 launch)
+cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st, int *cluster_used, int *launches,
+                         int jac_mode = JAC_CONVERGE) {
+  const bool vb = pa.fp_input == FP_DENSE_PAIR;  // B variants: always the round-2 kernels
+  if (inner_v1(pa.nmax) && !vb) {
+    pa.mode = PV_FULL;
+    ++*launches;
+    return launch_pivot(cx, pa, cluster_req, st, cluster_used);
+  }
+  const JacobiArgs j = jacobi_args(pa, jac_mode);
+  pa.prof = nullptr;
+  pa.mode = PV_PROLOGUE;
+  cudaError_t e = (factor_v1() && !vb) ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_prologue(cx, pa, st);
+  if (e != cudaSuccess) return e;
   JacShape sh = jacobi_default_shape(cx, pa.nmax, pa.count);
   if (cluster_req > 0 && cluster_req != sh.c && !jacobi_shape_for(pa.nmax, cluster_req, &sh))
     return cudaErrorInvalidConfiguration;  // no instantiated shape with that cluster size
@@ -185,6 +192,35 @@ cudaError_t launch_inner(bool cx, PivotArgs pa, int cluster_req, cudaStream_t st
   pa.mode = PV_EPILOGUE;
   *launches += 3;
   return (factor_v1() && !vb) ? launch_pivot(cx, pa, 0, st, nullptr) : launch_factor_epilogue(cx, pa, st);
+}
+
+// items [off, off + cnt) of a batch: every per-item array advanced by off
+PivotArgs sub_batch(const PivotArgs &pa, bool cx, int off, int cnt) {
+  const size_t w = cx ? 16 : 8;
+  PivotArgs s = pa;
+  s.items = pa.items + off;
+  s.count = cnt;
+  s.A = static_cast<char *>(pa.A) + size_t(off) * pa.bmax * pa.bmax * w;
+  s.D = pa.D + size_t(off) * 2 * pa.bmax;
+  s.W = static_cast<char *>(pa.W) + size_t(off) * pa.nmax * pa.nmax * w;
+  s.R0g = static_cast<char *>(pa.R0g) + size_t(off) * pa.nmax * pa.nmax * w;
+  s.stats = pa.stats + size_t(off) * ST_N;
+  s.dscr = pa.dscr ? static_cast<char *>(pa.dscr) + size_t(off) * pa.nmax * sizeof(double) : nullptr;
+  return s;
+}
+
+// Tail split of the Jacobi launch (HJB_TAIL_SPLIT=0 disables; A/B).  A batch
+// of `count` pivots on a GPU that holds `cap` of them at once runs
+// ceil(count / cap) waves; when the last wave is mostly empty (cfg5r: 128
+// pivots, 37 resident: 17 pivots on 68 of 148 SMs) those pivots go to a
+// second stream, and the epilogue and update of the full waves -- which only
+// need their own pivots -- run beside them on the idle SMs.
+bool tail_split_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("HJB_TAIL_SPLIT");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
 }
 
 struct PhaseCtx {
@@ -247,10 +283,6 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   pa.R0g = c.ws->R0.p;
   pa.dscr = c.ws->Dc.p;
   pa.fp_input = gram_items_d ? FP_DENSE_PAIR : FP_STRUCTURED;
-  int used = 0;
-  CK(launch_inner(c.cx, pa, c.cluster_req, c.st, &used, &c.launches, jac_mode));
-  c.cluster = used;
-  if (ev) CK(cudaEventRecord(ev[2], c.st));
   UpdateArgs u{};
   u.G = c.G;
   u.ldg = c.ld;
@@ -260,6 +292,47 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   u.nmax = c.nmax;
   u.W = c.ws->W.p;
   u.stats = stats_d;
+  // ---- tail split (see tail_split_enabled) ----
+  int n1 = count;
+  JacShape sh = jacobi_default_shape(c.cx, c.nmax, count);
+  if (tail_split_enabled() && !gram_items_d && !inner_v1(c.nmax) && !factor_v1() && c.cluster_req == 0 && !Rout &&
+      c.ws->stream2 && jac_mode == JAC_CONVERGE) {
+    const int cap = jacobi_wave_capacity(c.cx, c.nmax, sh);
+    if (cap > 0 && count > cap) {
+      const int tail = count % cap;
+      if (tail > 0 && 10 * tail <= 7 * cap) n1 = count - tail;  // last wave at most 70 % full
+    }
+  }
+  if (n1 < count) {
+    cudaStream_t s2 = c.ws->stream2;
+    CK(launch_factor_prologue(c.cx, pa, c.st));
+    CK(cudaEventRecord(c.ws->ev_fork, c.st));
+    CK(cudaStreamWaitEvent(s2, c.ws->ev_fork, 0));
+    const PivotArgs pa1 = sub_batch(pa, c.cx, 0, n1), pa2 = sub_batch(pa, c.cx, n1, count - n1);
+    CK(launch_jacobi(c.cx, jacobi_args(pa1, jac_mode), sh, c.st));
+    CK(launch_jacobi(c.cx, jacobi_args(pa2, jac_mode), sh, s2));
+    CK(launch_factor_epilogue(c.cx, pa1, c.st));
+    if (ev) CK(cudaEventRecord(ev[2], c.st));
+    UpdateArgs u1 = u, u2 = u;
+    u1.count = n1;
+    u2.items = items_d + n1;
+    u2.count = count - n1;
+    u2.W = static_cast<char *>(c.ws->W.p) + size_t(n1) * c.nmax * c.nmax * (c.cx ? 16 : 8);
+    u2.stats = stats_d + size_t(n1) * ST_N;
+    CK(launch_update(c.cx, u1, c.st));
+    CK(launch_factor_epilogue(c.cx, pa2, s2));
+    CK(launch_update(c.cx, u2, s2));
+    CK(cudaEventRecord(c.ws->ev_join, s2));
+    CK(cudaStreamWaitEvent(c.st, c.ws->ev_join, 0));
+    c.cluster = sh.c;
+    c.launches += 7;
+    if (ev) CK(cudaEventRecord(ev[3], c.st));
+    return HJB_OK;
+  }
+  int used = 0;
+  CK(launch_inner(c.cx, pa, c.cluster_req, c.st, &used, &c.launches, jac_mode));
+  c.cluster = used;
+  if (ev) CK(cudaEventRecord(ev[2], c.st));
   CK(launch_update(c.cx, u, c.st));
   ++c.launches;
   if (ev) CK(cudaEventRecord(ev[3], c.st));
@@ -494,6 +567,11 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   CK(cudaSetDevice(pr->device));
   Workspace &ws = g_ws[pr->device];
   if (!ws.stream) CK(cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking));
+  if (!ws.stream2) {
+    CK(cudaStreamCreateWithFlags(&ws.stream2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ws.ev_join, cudaEventDisableTiming));
+  }
   cudaStream_t st = pr->stream ? static_cast<cudaStream_t>(pr->stream) : ws.stream;
   const size_t w = esz(pr->dtype);
 
