@@ -464,6 +464,10 @@ def main():
         Gh = torch.from_numpy(np.ascontiguousarray(w.G.T)).pin_memory()  # pinned host, column-major
         Gh_np = Gh.numpy().T
         et = []
+        if sweep_mode:  # warm the page-locked result allocator (cfg1-3 do it with their untimed first solve)
+            from paper_1008_4166_b200 import _device
+            _warm = _device.pinned_host_colmajor(w.m, w.n, w.G.dtype)
+            del _warm
         reps = 1 if sweep_mode else args.steps + 1
         for k in range(reps):
             t0 = time.perf_counter()

@@ -67,6 +67,10 @@ typedef struct {
 #define HJB_FLAG_VARIANT_B 8     /* block-oriented variants 2B / 3B (parallel.py:160-174, 199-200):
                                     no F pre-pass, dense pair factor, one annihilation
                                     cycle per step; default: the F variants (2F / 3F) */
+#define HJB_FLAG_NO_TAIL_SPLIT 16 /* run the Jacobi launch of a step as one launch on the solve
+                                    stream (default: its last, mostly empty wave of pivots
+                                    runs on a second stream beside the update of the others;
+                                    same arithmetic, bitwise identical results) */
 #define HJB_FLAG_GATHER_ROOT 4   /* multi-GPU: only rank 0 receives the whole G_out
                                     (other ranks keep the blocks they hold);
                                     default: every rank receives it */
@@ -92,6 +96,7 @@ typedef struct {
   int64_t inner_sweeps;     /* sum of inner (pivot-level) sweeps over all pivots */
   int64_t inner_pair_visits;/* inner 2x2 pivots examined (sweeps * N(N-1)/2 per pivot) */
   int64_t kernel_launches;  /* kernels this library launched for the solve (this GPU) */
+  int64_t tail_splits;      /* steps whose Jacobi launch was split over two streams */
 } hjb_result;
 
 /* Library / ABI version (HJB_ABI_VERSION). */

@@ -23,6 +23,7 @@ HJB_HOST, HJB_DEVICE = 0, 1
 HJB_FLAG_PHASE_TIMES = 1
 HJB_FLAG_GATHER_ROOT = 4
 HJB_FLAG_VARIANT_B = 8
+HJB_FLAG_NO_TAIL_SPLIT = 16
 ST_N = 8
 
 
@@ -53,7 +54,7 @@ class Result(C.Structure):
         ("exchange_bytes", C.c_int64),
         ("cluster_size", C.c_int32), ("gram_splits", C.c_int32),
         ("inner_sweeps", C.c_int64), ("inner_pair_visits", C.c_int64),
-        ("kernel_launches", C.c_int64),
+        ("kernel_launches", C.c_int64), ("tail_splits", C.c_int64),
     ]
 
 

@@ -235,6 +235,8 @@ struct PhaseCtx {
   cudaStream_t st;
   int splits_used = 0;
   int launches = 0;  // kernels launched by this solve
+  bool tail_split = true;
+  int tail_splits = 0;  // steps whose Jacobi launch was split
 };
 
 // Gram -> pivot -> update for one batch of items (device item table).
@@ -295,7 +297,7 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
   // ---- tail split (see tail_split_enabled) ----
   int n1 = count;
   JacShape sh = jacobi_default_shape(c.cx, c.nmax, count);
-  if (tail_split_enabled() && !gram_items_d && !inner_v1(c.nmax) && !factor_v1() && c.cluster_req == 0 && !Rout &&
+  if (tail_split_enabled() && c.tail_split && !gram_items_d && !inner_v1(c.nmax) && !factor_v1() && c.cluster_req == 0 && !Rout &&
       c.ws->stream2 && jac_mode == JAC_CONVERGE) {
     const int cap = jacobi_wave_capacity(c.cx, c.nmax, sh);
     if (cap > 0 && count > cap) {
@@ -326,6 +328,7 @@ int run_phase(PhaseCtx &c, const Item *items_d, int count, int64_t *stats_d, voi
     CK(cudaStreamWaitEvent(c.st, c.ws->ev_join, 0));
     c.cluster = sh.c;
     c.launches += 7;
+    ++c.tail_splits;
     if (ev) CK(cudaEventRecord(ev[3], c.st));
     return HJB_OK;
   }
@@ -684,6 +687,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   ctx.max_sweeps = pr->max_sweeps;
   ctx.ws = &ws;
   ctx.st = st;
+  ctx.tail_split = !(pr->flags & HJB_FLAG_NO_TAIL_SPLIT);
   std::vector<int64_t> hstats(stats_per_sweep);
   double tg = 0, tp = 0, tu = 0, tx = 0;
 
@@ -859,6 +863,7 @@ int hjb_solve(const hjb_problem *pr, hjb_result *res) {
   res->cluster_size = ctx.cluster;
   res->gram_splits = ctx.splits_used;
   res->kernel_launches = ctx.launches;
+  res->tail_splits = ctx.tail_splits;
   return HJB_OK;
 }
 

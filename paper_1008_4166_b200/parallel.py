@@ -69,6 +69,7 @@ class SolverConfig:
     gather_root: bool = False
     first_sweep: int = 1
     sweep_count: int = 0
+    tail_split: bool = True   # False: HJB_FLAG_NO_TAIL_SPLIT (one Jacobi launch per step)
 
     def __post_init__(self):
         if self.variant not in VARIANTS:
@@ -107,7 +108,8 @@ def _problem(cfg: SolverConfig, m, n, ld, cx, mem, gin, gout, signs, device, str
     pr.comm = cfg.comm.handle if cfg.comm is not None else None
     pr.flags = (_lib.HJB_FLAG_PHASE_TIMES if cfg.phase_times else 0) | \
         (_lib.HJB_FLAG_GATHER_ROOT if cfg.gather_root else 0) | \
-        (_lib.HJB_FLAG_VARIANT_B if cfg.variant in ("2B", "3B") else 0)
+        (_lib.HJB_FLAG_VARIANT_B if cfg.variant in ("2B", "3B") else 0) | \
+        (0 if cfg.tail_split else _lib.HJB_FLAG_NO_TAIL_SPLIT)
     pr.first_sweep = cfg.first_sweep
     pr.sweep_count = cfg.sweep_count
     return pr

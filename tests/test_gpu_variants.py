@@ -201,3 +201,30 @@ def test_ragged_shapes_every_kernel_instance(cx, n, m, p, variant, strategy):
     res = pkg.extract_eigen(Gout, J)
     lam = res.eigenvalues.cpu().numpy() if hasattr(res.eigenvalues, "cpu") else np.asarray(res.eigenvalues)
     assert np.all(np.sign(lam) == J)
+
+
+def test_tail_split_is_bitwise_neutral():
+    """A step with more pivots than resident Jacobi clusters splits its last,
+    mostly empty wave onto a second stream (solver.cu run_phase).  Same
+    arithmetic: G_out is bitwise equal to the single-launch run."""
+    import torch
+    from paper_1008_4166_b200 import parallel as par
+    rng = np.random.default_rng(21)
+    p, b, m = 20, 66, 700          # 20 pivots of order 132 -> the order-256 complex instance (18 resident)
+    n = 2 * p * b
+    G = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    # m < n would be rank deficient: use a tall factor instead
+    m = n + 8
+    G = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    J = np.array([1] * (n // 2) + [-1] * (n - n // 2), np.int8)
+    Gd = torch.from_numpy(np.ascontiguousarray(G.T)).cuda().t()
+    outs, res = [], []
+    for split in (True, False):
+        cfg = pkg.SolverConfig(variant="2F", strategy="round_robin", p=p, tol=pkg.Tolerances(orth_tol=n * EPS),
+                               tail_split=split, sweep_count=2)
+        out = torch.empty_like(Gd.t()).t()
+        res.append(par.solve_device(Gd, J, cfg, out=out))
+        outs.append(out)
+    assert res[0].tail_splits > 0 and res[1].tail_splits == 0
+    assert res[0].rotations == res[1].rotations
+    assert torch.equal(outs[0], outs[1])
