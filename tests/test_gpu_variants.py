@@ -228,3 +228,15 @@ def test_tail_split_is_bitwise_neutral():
     assert res[0].tail_splits > 0 and res[1].tail_splits == 0
     assert res[0].rotations == res[1].rotations
     assert torch.equal(outs[0], outs[1])
+
+
+def test_randomised_shapes_against_the_oracle():
+    """60 seeded random small problems (tools/fuzz_gpu.py: both dtypes, variants
+    and orderings, ragged blocks down to width 1, graded columns, any inertia)
+    agree with the oracle; 300 more were run once per round (profiles/)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "fuzz_gpu", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "fuzz_gpu.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.run(60, 7) == 0
