@@ -1,16 +1,21 @@
 // Host driver and C ABI of hjb200 (include/hjb200.h).
 //
 // hjb_solve replaces the reference's parallel_jacobi (pkg/src/hjacobi/
-// parallel.py:255-309) for variant 2F.  The P ring workers become the CTA
-// clusters of one batched launch per phase; the ring exchange of the
-// reference (parallel.py:212-221) is an index remap on one GPU (every block
-// keeps its column position in the device copy of G) and an NCCL send/recv of
-// the blocks that cross a GPU boundary with several GPUs.  Per sweep:
-//   pre-pass: Gram(diag) -> pivot(dense) -> update        (parallel.py:138-148)
-//   steps:    Gram(pair) -> pivot(structured) -> update   (parallel.py:185-210)
-//             [-> NCCL block exchange]                     (parallel.py:212-221)
+// parallel.py:255-309), F variants by default and B variants with
+// HJB_FLAG_VARIANT_B.  The P ring workers become the items of one batched
+// launch per phase; the ring exchange of the reference (parallel.py:212-221)
+// is an index remap on one GPU (every block keeps its column position in the
+// device copy of G) and an NCCL send/recv of the blocks that cross a GPU
+// boundary with several GPUs.  Per sweep:
+//   F pre-pass: Gram(diag) -> factor -> Jacobi -> W -> update  (parallel.py:138-148)
+//   steps:      Gram(pair) -> factor (structured; B: dense pair) -> Jacobi
+//               (F: to convergence; B: one cycle) -> W = R0^-1 R_final -> update
+//                                                              (parallel.py:185-210)
+//               [-> NCCL block exchange]                       (parallel.py:212-221)
 //   one host read of the per-item counters, all-reduced over GPUs
-//                                                          (parallel.py:239-244)
+//                                                              (parallel.py:239-244)
+// Pivots of order <= 64 use the single cluster pivot kernel of round 1
+// (pivot.cu) instead of factor / Jacobi / factor (inner_v1).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
