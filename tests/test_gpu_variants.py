@@ -240,3 +240,18 @@ def test_randomised_shapes_against_the_oracle():
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     assert mod.run(60, 7) == 0
+
+
+def test_c_example_runs_on_the_gpu(tmp_path):
+    """examples/solve_c.c (plain C caller of the ABI) solves its problem."""
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    libdir = os.path.join(root, "paper_1008_4166_b200")
+    exe = str(tmp_path / "solve_c")
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(root, "include"), os.path.join(root, "examples", "solve_c.c"),
+                    "-o", exe, "-L", libdir, "-l:libhjb200.so", f"-Wl,-rpath,{libdir}", "-lm"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "converged 1" in r.stdout, (r.stdout, r.stderr)

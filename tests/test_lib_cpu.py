@@ -123,3 +123,28 @@ def test_native_partition_matches_reference_rule():
                 continue
             assert list(P.uniform_partition(n, nbl).sizes) == O.uniform_sizes(n, nbl)
     assert P.greedy_partition(10, 4).sizes == (4, 4, 2) and P.num_blocks(10, 4) == 3
+
+
+def test_header_is_plain_c_and_the_c_example_links(tmp_path):
+    """include/hjb200.h is a C header (plain pointers and sizes, no C++ / torch
+    types): examples/solve_c.c compiles as C99 with -Werror and links against
+    the built library; every symbol the header declares resolves.  Without a
+    GPU the program stops at hjb_device_count() (exit 2, "no CPU fallback")."""
+    import re
+    import shutil
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    libdir = os.path.join(root, "paper_1008_4166_b200")
+    exe = str(tmp_path / "solve_c")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "solve_c.c"), "-o", exe, "-L", libdir, "-l:libhjb200.so",
+                    f"-Wl,-rpath,{libdir}", "-lm"], check=True)
+    header = open(os.path.join(root, "include", "hjb200.h")).read()
+    declared = set(re.findall(r"^(?:int|const char \*)\s*(hjb_\w+)\(", header, re.M))
+    assert declared and declared <= set(_lib.SIGNATURES), declared - set(_lib.SIGNATURES)
+    if _lib.lib().hjb_device_count() < 1:
+        r = subprocess.run([exe], capture_output=True, text=True)
+        assert r.returncode == 2 and "no CPU fallback" in r.stderr
