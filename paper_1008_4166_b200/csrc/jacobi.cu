@@ -50,6 +50,9 @@ namespace cg = cooperative_groups;
 #ifndef HJB_JAC_PROF
 #define HJB_JAC_PROF 0
 #endif
+#ifndef HJB_JAC_MINB_SMALL  // resident CTAs per SM for 4-warp CTAs of pivots of order <= 128
+#define HJB_JAC_MINB_SMALL 3
+#endif
 #ifndef HJB_JAC_FUSE  // 1: gather-first + fused next-round dots (slower on B200: register pressure)
 #define HJB_JAC_FUSE 0
 #endif
@@ -789,7 +792,7 @@ template <typename T, int N, int C, int W, int SPW>
 static cudaError_t launch_jacobi_t(const JacobiArgs &a, cudaStream_t st) {
   using Cfg = JacCfg<T, N, C, W, SPW>;
   // two CTAs per SM for 4-warp CTAs (255 registers per thread either way)
-  constexpr int MINB = Cfg::NT <= 128 ? 2 : 1;
+  constexpr int MINB = Cfg::NT <= 128 ? (N <= 128 ? HJB_JAC_MINB_SMALL : 2) : 1;
   auto k = jacobi_kernel<T, N, C, W, SPW, MINB>;
   static DeviceFlags attr_flags;
   bool *attr = attr_flags.here();
@@ -879,7 +882,7 @@ cudaError_t launch_jacobi(bool cx, const JacobiArgs &a, JacShape s, cudaStream_t
 template <typename T, int N, int C, int W, int SPW>
 static int query_jacobi_t() {
   using Cfg = JacCfg<T, N, C, W, SPW>;
-  constexpr int MINB = Cfg::NT <= 128 ? 2 : 1;
+  constexpr int MINB = Cfg::NT <= 128 ? (N <= 128 ? HJB_JAC_MINB_SMALL : 2) : 1;
   auto k = jacobi_kernel<T, N, C, W, SPW, MINB>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)) != cudaSuccess) return 0;
   if (C > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return 0;
