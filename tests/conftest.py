@@ -17,6 +17,19 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
 
 
+def pytest_sessionstart(session):
+    """A fresh checkout has no libhjb200.so (built artefacts stay out of
+    history): build it once (nvcc cross-compiles sm_100a without a GPU, about
+    two minutes) so the library tests do not fail on "not built".  An
+    up-to-date library is left alone."""
+    try:
+        from paper_1008_4166_b200 import build as b
+        if not os.environ.get("HJB_LIB"):
+            b.build(force=False)
+    except Exception as exc:  # the tests that need the library will say so loudly
+        sys.stderr.write(f"conftest: library build skipped/failed: {exc}\n")
+
+
 @pytest.fixture
 def rng():
     # the reference suite's seed (pkg/tests/conftest.py:5-7)
