@@ -20,12 +20,13 @@ def pytest_configure(config):
 def pytest_sessionstart(session):
     """A fresh checkout has no libhjb200.so (built artefacts stay out of
     history): build it once (nvcc cross-compiles sm_100a without a GPU, about
-    two minutes) so the library tests do not fail on "not built".  An
-    up-to-date library is left alone."""
+    two minutes) so the library tests do not fail on "not built".  An existing
+    library is left alone (a copied tree has unreliable mtimes; rebuild with
+    ``python -m paper_1008_4166_b200.build`` or ``__graft_entry__.build()``)."""
     try:
         from paper_1008_4166_b200 import build as b
-        if not os.environ.get("HJB_LIB"):
-            b.build(force=False)
+        if not os.environ.get("HJB_LIB") and not os.path.exists(b.OUT):
+            b.build(force=True)
     except Exception as exc:  # the tests that need the library will say so loudly
         sys.stderr.write(f"conftest: library build skipped/failed: {exc}\n")
 
