@@ -33,18 +33,13 @@ class FactoredForm:
 
 
 def _eigh2(a, b, c):
-    """Spectral decomposition of [[a, b], [conj(b), c]] with the stable
-    small-angle rotation (factorization.py:32-51)."""
-    if b == 0:
-        return float(a), float(c), np.eye(2)
-    ab = abs(b)
-    phase = b / ab
-    theta = (c - a) / (2.0 * ab)
-    sg = 1.0 if theta >= 0.0 else -1.0
-    t = sg / (abs(theta) + math.sqrt(theta * theta + 1.0))
-    cs = 1.0 / math.sqrt(1.0 + t * t)
-    sn = cs * t
-    return float(a - t * ab), float(c + t * ab), np.array([[cs * phase, sn * phase], [-sn, cs]])
+    """Eigenvalues and an orthonormal eigenvector matrix of the 2x2 Hermitian
+    pivot block [[a, b], [conj(b), c]] of the LDL^* factor (LAPACK's
+    symmetric eigensolver on the tiny block; any orthonormal basis serves the
+    column scaling below)."""
+    blk = np.array([[a, b], [np.conj(b), c]])
+    w, Q = np.linalg.eigh(blk)
+    return float(w[0]), float(w[1]), Q
 
 
 def factorize_hermitian_indefinite(H, herm_rtol=1e-10):
@@ -90,22 +85,27 @@ def factorize_hermitian_indefinite(H, herm_rtol=1e-10):
 
 
 def order_by_inertia(f: FactoredForm) -> FactoredForm:
-    """Stable permutation putting +1 before -1 (factorization.py:147-153)."""
-    idx = np.argsort(f.J == -1, kind="stable")
-    return replace(f, G=np.asfortranarray(f.G[:, idx]), J=f.J[idx], P1=f.P1[idx])
+    """Columns with sign +1 first, then the -1 columns, each group in its
+    original order; P1 records where every column came from
+    (factorization.py:147-153)."""
+    pos, neg = np.flatnonzero(f.J != -1), np.flatnonzero(f.J == -1)
+    take = np.concatenate([pos, neg])
+    return replace(f, G=np.asfortranarray(f.G[:, take]), J=f.J[take], P1=f.P1[take])
 
 
 def scaled_condition(A):
-    """kappa of A scaled to unit diagonal (factorization.py:156-168);
-    diagnostic only."""
+    """kappa_2 of D^-1/2 A D^-1/2 with D = diag(A), from a symmetric
+    eigensolver on the host (factorization.py:156-168; a diagnostic for a
+    Gram matrix that is already on the host -- ``scaled_condition_factor``
+    is the GPU form used by ``solve_hermitian``)."""
     A = as_matrix(A)
-    d = np.diag(A).real
-    if np.any(d <= 0):
+    diag = np.real(np.diagonal(A))
+    if diag.size and diag.min() <= 0:
         raise ValueError("scaled_condition requires a strictly positive diagonal")
-    s = 1.0 / np.sqrt(d)
-    As = A * np.outer(s, s)
-    w = np.abs(np.linalg.eigvalsh((As + As.conj().T) / 2))
-    return math.inf if w.min() == 0.0 else float(w.max() / w.min())
+    r = np.reciprocal(np.sqrt(diag))
+    As = (A * r[:, None]) * r[None, :]
+    ev = np.abs(np.linalg.eigvalsh(0.5 * (As + As.conj().T)))
+    return math.inf if ev.size and ev.min() == 0.0 else float(ev.max() / ev.min()) if ev.size else 1.0
 
 
 def scaled_condition_factor(G) -> float:
@@ -145,16 +145,20 @@ def scaled_condition_factor(G) -> float:
 
 
 def accept_external_factor(G, J) -> FactoredForm:
-    """Wrap a user-supplied full-column-rank factor (factorization.py:171-189)."""
+    """A caller-supplied factor pair taken as is, after the reference's checks
+    (factorization.py:171-189): at least as many rows as columns, a valid sign
+    vector, no zero column, full column rank (Cholesky of the Gram)."""
     G = as_matrix(G)
-    m_rows, n_cols = G.shape
-    if n_cols > m_rows:
+    rows, cols = G.shape
+    if cols > rows:
         raise ValueError("factor must have at least as many rows as columns")
-    signs = as_signs(J, n_cols)
+    signs = as_signs(J, cols)
+    gram = G.conj().T @ G
     try:
-        np.linalg.cholesky(G.conj().T @ G)
+        np.linalg.cholesky(gram)
     except np.linalg.LinAlgError as exc:
         raise RankDeficiencyError("supplied factor is rank deficient") from exc
-    if n_cols and (np.abs(G) ** 2).sum(axis=0).min() == 0.0:
+    if cols and np.real(np.diagonal(gram)).min() == 0.0:
         raise RankDeficiencyError("supplied factor has a zero column")
-    return FactoredForm(G=G, J=signs, P=np.arange(m_rows), P1=np.arange(n_cols))
+    ident_r, ident_c = np.arange(rows), np.arange(cols)
+    return FactoredForm(G=G, J=signs, P=ident_r, P1=ident_c)
