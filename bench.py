@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg5r")
+    ap.add_argument("--variant", default="2F", choices=["2F", "3F", "2B", "3B"],
+                    help="ring variant (parallel.py:43); the metric's line is 2F")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
@@ -165,16 +167,19 @@ def add_stats(acc, res):
     return acc
 
 
-def flops_of(stats, w, cx):
+def flops_of(stats, w, cx, variant="2F"):
     """SURVEY.md 8(d) algorithmic FLOPs (Gram + update, the headline) and
-    the inner-level (pivot) flops reported separately."""
+    the inner-level (pivot) flops reported separately.  B variants: three Gram
+    products per pair (A_ii, A_jj, A_ij of the dense pair Gram), no pre-pass."""
     from paper_1008_4166_b200 import workloads
     b = w.b
     c = 4.0 if cx else 1.0
-    gram = c * 2.0 * w.m * b * b * (stats["pairs_visited"] + stats["prepass_visited"])
+    gpp = 3.0 if variant.endswith("B") else 1.0
+    gram = c * 2.0 * w.m * b * b * (gpp * stats["pairs_visited"] + stats["prepass_visited"])
     upd = c * (8.0 * w.m * b * b * stats["pairs_updated"] + 2.0 * w.m * b * b * stats["prepass_updated"])
     total = workloads.algorithmic_flops(w.m, b, cx, stats["pairs_updated"], stats["pairs_visited"],
                                         stats["prepass_updated"], stats["prepass_visited"])
+    total += c * 2.0 * w.m * b * b * (gpp - 1.0) * stats["pairs_visited"]
     # inner level: a dot product (2N real flops, x4 complex) per examined 2x2
     # pivot and 6N (x4 complex) per applied rotation on R (W is formed once)
     N = 2 * b
@@ -329,7 +334,7 @@ def main():
     cx = np.iscomplexobj(w.G)
     sweep_mode = w.name in SWEEP_STEP_CONFIGS
     tol = P.Tolerances(orth_tol=w.orth_tol)
-    cfg_solve = P.SolverConfig(variant="2F", strategy="round_robin", p=w.p, tol=tol, comm=comm)
+    cfg_solve = P.SolverConfig(variant=args.variant, strategy="round_robin", p=w.p, tol=tol, comm=comm)
     signs = np.ascontiguousarray(w.J, np.int8)
     G0 = torch.from_numpy(np.ascontiguousarray(w.G.T)).to(dev).t()  # column-major, resident
     Gw = torch.empty_like(G0.t()).t()
@@ -349,8 +354,8 @@ def main():
         """One outer sweep of the running solve; returns its result."""
         if state["k"] == 1:
             Gw.copy_(G0)
-        cfg = P.SolverConfig(variant="2F", strategy="round_robin", p=w.p, tol=tol, comm=comm, phase_times=True,
-                             first_sweep=state["k"], sweep_count=1)
+        cfg = P.SolverConfig(variant=args.variant, strategy="round_robin", p=w.p, tol=tol, comm=comm,
+                             phase_times=True, first_sweep=state["k"], sweep_count=1)
         r = par.solve_device(Gw, signs, cfg, out=Gw)
         done = bool(r.converged) or state["k"] >= max_sw
         state["k"] = 1 if done else state["k"] + 1
@@ -419,15 +424,15 @@ def main():
         add_stats(stats, r)
     if not sweep_mode:
         # phase split from a separate untimed run with per-phase events
-        pt = par.solve_device(G0, signs, P.SolverConfig(variant="2F", strategy="round_robin", p=w.p, tol=tol,
-                                                        comm=comm, phase_times=True), out=Gw)
+        pt = par.solve_device(G0, signs, P.SolverConfig(variant=args.variant, strategy="round_robin", p=w.p,
+                                                        tol=tol, comm=comm, phase_times=True), out=Gw)
         stats = add_stats({}, pt)
     elif Gsave is not None:
         Gw.copy_(Gsave)
         del Gsave
     phase = {"gram_ms": stats["t_gram_ms"], "pivot_ms": stats["t_pivot_ms"], "update_ms": stats["t_update_ms"],
              "exchange_ms": stats["t_exchange_ms"]}
-    total_f, gram_f, upd_f, piv_f = flops_of(stats, w, cx)
+    total_f, gram_f, upd_f, piv_f = flops_of(stats, w, cx, args.variant)
     if pg is not None:  # every rank counts its own pairs: sum
         ft = torch.tensor([total_f, gram_f, upd_f, piv_f], dtype=torch.float64)
         pg.all_reduce(ft)
@@ -495,7 +500,7 @@ def main():
                 "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
                 "dtype": "c128" if cx else "f64", "data": "synthetic (seeded, BASELINE.json generators)",
                 "config": {"workload": w.name, "m": w.m, "n": w.n, "b": w.b, "p": w.p,
-                           "strategy": "round_robin", "orth_tol": "n*eps", "step": step_desc,
+                           "variant": args.variant, "strategy": "round_robin", "orth_tol": "n*eps", "step": step_desc,
                            "l2": ("inputs larger than L2 (no flush)" if flush is None
                                   else "flushed (256 MiB write) between timed steps"),
                            "parallelism": f"ring p={w.p} over {world} GPU(s)"},

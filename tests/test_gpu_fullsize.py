@@ -124,3 +124,29 @@ def test_full_size_vs_reference(pkg, name, kw, key):
     assert math.isfinite(m["j_orth_loss"])
     if name != "cfg3":
         assert m["j_orth_loss"] <= 64 * w.n * EPS * kappa, m
+
+
+def test_cfg2_full_size_block_oriented_variant(pkg):
+    """The B variant at the full size of cfg2: same eigenvalues as the
+    reference's 2F run (the spectrum does not depend on the variant), residual,
+    orthogonality and preservation of H within the north-star bounds."""
+    import torch
+
+    from paper_1008_4166_b200 import parallel as par
+    from paper_1008_4166_b200 import workloads
+
+    key = "cfg2_n2048_b64"
+    z = golden(f"fullsize_{key}.npz")
+    kappa = float(z[key + "_info"][6])
+    w = workloads.make("cfg2")
+    cfg = pkg.SolverConfig(variant="2B", strategy="round_robin", p=w.p, tol=pkg.Tolerances(orth_tol=w.orth_tol))
+    Gd = torch.from_numpy(np.ascontiguousarray(w.G.T)).cuda().t()
+    out = torch.empty_like(Gd.t()).t()
+    r = par.solve_device(Gd, np.ascontiguousarray(w.J, np.int8), cfg, out=out)
+    m = metrics_gpu(w.G, w.J, out, np.sort(z[key + "_lam"]), kappa)
+    print(json.dumps(dict(m, sweeps=r.sweeps, rotations=r.rotations, solve_ms=r.t_total_ms)))
+    assert r.converged and r.prepass_visited == 0
+    assert m["max_rel_eig"] <= m["eig_bound"], m
+    assert m["residual"] <= m["residual_bound"], m
+    assert m["orthogonality"] <= m["orth_bound"], m
+    assert m["h_preservation"] <= 64 * w.n * EPS, m
